@@ -1,0 +1,389 @@
+"""Headline benchmark: work_oriented (merge-path) SpMV on a 2^24-row R-MAT CSR, fp32.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--schedule work_oriented|thread_mapped|group_warp|group_block]
+                    [--scale 24] [--dtype fp32|fp64]
+
+One step = one y = A x over the whole matrix with inputs resident in HBM (the
+matrix is 2.2 GB fp32, far larger than the 126 MB L2, so no flush is needed
+between steps; x (64 MB) may stay L2-resident across steps, as it would in an
+iterated SpMV). Timed with CUDA events on the launching stream, bracketed by a
+barrier + synchronize, max over ranks. Metric = GFLOP/s = 2*nnz / t.
+
+N > 1 (torchrun, one rank per GPU): the same matrix is built on every rank,
+split into nnz-balanced row shards (x replicated) and each rank times its own
+shard; value = 2*nnz_total / max_rank(t) — total work fixed, "scaling": "strong".
+
+--impl reference times the reference's CPU algorithm (the C oracle port of
+lanework's numba merge-path loop, fp64/int64 like the reference, all host
+threads, lanes = 32 x threads — the reference CLI's configuration) on the same
+matrix generated on the host; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "SpMV GFLOP/s (work_oriented merge-path, fp32, 2^24-row R-MAT CSR)"
+PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
+FALLBACK_HBM = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--schedule", default="work_oriented",
+                    choices=["work_oriented", "thread_mapped", "group_warp", "group_block"])
+    ap.add_argument("--scale", type=int, default=24)
+    ap.add_argument("--edge-factor", type=int, default=16)
+    ap.add_argument("--seed", type=int, default=3)
+    ap.add_argument("--dtype", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--cpu-reps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        d = json.loads(PEAKS_FILE.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self._t = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------
+def reference_arm(args):
+    """Reference CPU algorithm (oracle port), rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import oracle
+    from paper_2301_04792_b200.sparse import rmat_thresholds
+
+    threads = oracle.default_threads()
+    t0 = time.time()
+    off, col, val = oracle.rmat_csr(args.scale, args.edge_factor, args.seed, rmat_thresholds(),
+                                    threads=threads)
+    if args.dtype == "fp32":
+        val = val.astype(np.float32).astype(np.float64)
+    gen_s = time.time() - t0
+    rows = off.size - 1
+    nnz = int(off[-1])
+    x = np.ones(rows, dtype=np.float64)
+    lanes = 32 * threads
+    for _ in range(args.warmup):
+        oracle.spmv(off, col, val, x, "merge-path", lanes=lanes, threads=threads)
+    times = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        oracle.spmv(off, col, val, x, "merge-path", lanes=lanes, threads=threads)
+        times.append(time.perf_counter() - t)
+    sec = float(np.mean(times))
+    gflops = 2.0 * nnz / sec / 1e9
+    sample = (f"full R-MAT scale {args.scale} matrix ({rows} rows, {nnz} nnz), merge-path, "
+              f"fp64/int64, {threads} threads, {lanes} lanes, mean of {args.steps} runs")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gflops, 4), "unit": "GFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"rmat{args.scale}-ef{args.edge_factor}-seed{args.seed}",
+                   "schedule": "merge-path", "rows": rows, "nnz": nnz},
+        "cpu_baseline": {"value": round(gflops, 4), "unit": "GFLOP/s", "cores": threads,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": round(gflops, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "generation_s": round(gen_s, 2),
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------
+def our_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2301_04792_b200 as lwb
+    from paper_2301_04792_b200 import _lib
+    from paper_2301_04792_b200.device import current_stream
+    from paper_2301_04792_b200.distributed import nnz_balanced_bounds
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    dtype = "float32" if args.dtype == "fp32" else "float64"
+    full = lwb.generate_rmat_csr(args.scale, args.edge_factor, args.seed, dtype=dtype, device=dev)
+    nnz_total = full.nnz
+    rows_total = full.rows
+    if world > 1:
+        bounds = nnz_balanced_bounds(full.row_offsets.cpu().numpy(), world)
+        A = full.row_slice(int(bounds[rank]), int(bounds[rank + 1]))
+        A = lwb.DeviceCsr(A.rows, A.cols, A.row_offsets.clone(), A.col_indices.clone(),
+                          A.values.clone())
+        del full
+        torch.cuda.empty_cache()
+    else:
+        A = full
+    x = torch.ones(A.cols, dtype=A.dtype, device=dev)
+    y = torch.empty(A.rows, dtype=A.dtype, device=dev)
+
+    sched = {"work_oriented": lwb.ScheduleKind.MERGE_PATH,
+             "thread_mapped": lwb.ScheduleKind.THREAD_MAPPED,
+             "group_warp": lwb.ScheduleKind.GROUP_MAPPED,
+             "group_block": lwb.ScheduleKind.GROUP_MAPPED}[args.schedule]
+    gs = 256 if args.schedule == "group_block" else 32
+    cfg = lwb.ExecutorConfig(schedule=sched, group_size=gs)
+    lib = _lib.load()
+    Ac = A.c_struct()
+    stream = torch.cuda.current_stream(dev)
+    sp = current_stream(dev)
+    ws_bytes = lib.lw_spmv_workspace(_lib.LW_MERGE_PATH, A.rows, A.nnz, 0, Ac.dtype)
+    ws = torch.empty(max(ws_bytes, 256), dtype=torch.uint8, device=dev)
+    launches_per_step = 3 if sched is lwb.ScheduleKind.MERGE_PATH else 1
+
+    # one step, with the dominant kernel bracketed by events
+    ev = []
+
+    def step(record):
+        if sched is lwb.ScheduleKind.MERGE_PATH:
+            _lib.check(lib.lw_spmv_work_oriented_phases(Ac, x.data_ptr(), y.data_ptr(), 0,
+                                                        ws.data_ptr(), ws.numel(), 1, sp), "p1")
+            if record:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            _lib.check(lib.lw_spmv_work_oriented_phases(Ac, x.data_ptr(), y.data_ptr(), 0,
+                                                        ws.data_ptr(), ws.numel(), 2, sp), "p2")
+            if record:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record(stream)
+                ev.append((e0, e1))
+            _lib.check(lib.lw_spmv_work_oriented_phases(Ac, x.data_ptr(), y.data_ptr(), 0,
+                                                        ws.data_ptr(), ws.numel(), 4, sp), "p3")
+        else:
+            if record:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            lwb.spmv(A, x, cfg, out=y)
+            if record:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record(stream)
+                ev.append((e0, e1))
+
+    for _ in range(max(args.warmup, 3)):
+        step(False)
+    torch.cuda.synchronize()
+    # pass A: whole steps timed back to back (the headline value)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            step(False)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms_total = t0.elapsed_time(t1)
+    # pass B: same steps with the dominant kernel bracketed (events add a little gap)
+    ev.clear()
+    for _ in range(args.steps):
+        step(True)
+    torch.cuda.synchronize()
+    kern_ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+
+    ms = ms_total / args.steps
+    if world > 1:
+        t = torch.tensor([ms, kern_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, kern_ms = float(t[0]), float(t[1])
+    gflops = 2.0 * nnz_total / (ms * 1e-3) / 1e9
+
+    # algorithmic bytes of the dominant kernel for this rank's shard
+    alg_bytes = A.algorithmic_bytes()
+    hbm, hbm_src = peaks()
+    achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": round(gflops, 3), "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32" if args.dtype == "fp32" else "f64", "data": "synthetic",
+        "config": {"workload": f"rmat{args.scale}-ef{args.edge_factor}-seed{args.seed}",
+                   "schedule": args.schedule, "rows": rows_total, "nnz": nnz_total,
+                   "parallelism": f"rows{world}" if world > 1 else "single",
+                   "l2": "inputs > L2 (2.2 GB matrix streamed per step); no flush"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
+                     "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": None,
+                     "kernel": "k_wo_staged" if sched is lwb.ScheduleKind.MERGE_PATH else args.schedule,
+                     "kernel_ms": round(kern_ms, 4), "alg_bytes": alg_bytes,
+                     "peak_source": hbm_src, "frac_of_8TBps": round(achieved / 8000.0, 4)},
+        "hbm_gbs_step": round(alg_bytes / (ms * 1e-3) / 1e9, 1),
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clocks.summary(),
+    }
+
+    # e2e: reference-facing C-ABI call with HOST buffers (pinned), copies inside
+    if not args.no_e2e and world == 1:
+        line["e2e"] = e2e_host(A, args, lib, dev, nnz_total)
+    if not args.no_cpu_baseline and rank == 0 and world == 1:
+        line["cpu_baseline"] = cpu_baseline(A, args)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_host(A, args, lib, dev, nnz_total):
+    import torch
+
+    from paper_2301_04792_b200 import _lib
+
+    h_off = A.row_offsets.cpu().pin_memory()
+    h_col = A.col_indices.cpu().pin_memory()
+    h_val = A.values.cpu().pin_memory()
+    h_x = torch.ones(A.cols, dtype=A.dtype).pin_memory()
+    h_y = torch.empty(A.rows, dtype=A.dtype).pin_memory()
+    H = _lib.LwCsr()
+    H.rows, H.cols, H.nnz = A.rows, A.cols, A.nnz
+    H.row_offsets, H.col_indices, H.values = h_off.data_ptr(), h_col.data_ptr(), h_val.data_ptr()
+    H.offset_bits, H.dtype = A.offset_bits, A.c_struct().dtype
+    stream = torch.cuda.current_stream(dev)
+    sp = int(stream.cuda_stream)
+    steps = max(2, min(args.steps, 5))
+    for _ in range(2):
+        _lib.check(lib.lw_spmv_host(_lib.LW_MERGE_PATH, H, h_x.data_ptr(), h_y.data_ptr(), 0, 32,
+                                    32, sp), "lw_spmv_host")
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(steps):
+        _lib.check(lib.lw_spmv_host(_lib.LW_MERGE_PATH, H, h_x.data_ptr(), h_y.data_ptr(), 0, 32,
+                                    32, sp), "lw_spmv_host")
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    h2d = (h_off.numel() * h_off.element_size() + h_col.numel() * 4
+           + h_val.numel() * h_val.element_size() + h_x.numel() * h_x.element_size())
+    return {"value": round(2.0 * nnz_total / (ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(h_y.numel() * h_y.element_size()),
+            "ms_per_step": round(ms, 3), "steps": steps,
+            "path": "lw_spmv_host (C ABI, pinned host CSR + x in, y out, stream-synchronized)"}
+
+
+def cpu_baseline(A, args):
+    """Reference CPU algorithm (oracle port of lanework merge-path, fp64) on the same matrix."""
+    from oracle import oracle
+
+    threads = oracle.default_threads()
+    off = A.row_offsets.cpu().numpy().astype(np.int64)
+    col = A.col_indices.cpu().numpy().astype(np.int64)
+    val = A.values.cpu().numpy().astype(np.float64)
+    x = np.ones(A.cols)
+    lanes = 32 * threads
+    oracle.spmv(off, col, val, x, "merge-path", lanes=lanes, threads=threads)
+    times = []
+    for _ in range(args.cpu_reps):
+        t = time.perf_counter()
+        oracle.spmv(off, col, val, x, "merge-path", lanes=lanes, threads=threads)
+        times.append(time.perf_counter() - t)
+    sec = float(np.median(times))
+    return {"value": round(2.0 * A.nnz / sec / 1e9, 4), "unit": "GFLOP/s", "cores": threads,
+            "kind": "port", "ms_per_step": round(sec * 1e3, 2),
+            "sample": (f"full matrix ({A.rows} rows, {A.nnz} nnz), oracle port of lanework "
+                       f"merge-path (fp64/int64), {lanes} lanes on {threads} threads, median of "
+                       f"{args.cpu_reps}")}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        our_arm(args)
+
+
+if __name__ == "__main__":
+    main()

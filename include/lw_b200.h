@@ -1,0 +1,181 @@
+/*
+ * lw_b200.h — C ABI of the B200-native load-balanced SpMV library (liblwb200.so).
+ *
+ * This is the drop-in boundary for the reference's compiled SpMV loops. The
+ * reference (`lanework` 0.1.0, /root/reference/pkg/src/lanework) has no FFI: its
+ * "plugin" seam is the backend switch in _backend.py:24-66 and the three numba
+ * entry points in _fast.py that take raw arrays and return nothing. Every entry
+ * point below names the reference interface it replaces.
+ *
+ * Conventions
+ *   - Every pointer inside lw_csr_t / lw_probe_t and every x/y/workspace pointer
+ *     is a DEVICE pointer owned by the caller (e.g. a torch CUDA tensor). The only
+ *     exceptions are the *_host entry points, documented where they appear.
+ *   - `stream` is a cudaStream_t passed as uintptr_t (0 = legacy default stream).
+ *     All device entry points are stream-ordered and reentrant; none allocates
+ *     memory behind the caller's back (workspace sizes come from *_workspace()).
+ *   - Return value: 0 on success, otherwise a cudaError_t value (< 10000) or an
+ *     LW_E_* code (>= 10000). lw_error_string() maps either to text.
+ *   - Arithmetic: products and sums are carried in fp64 for both fp32 and fp64
+ *     inputs; y is rounded to the input dtype once per row (plus once per carry
+ *     fix-up for rows a work_oriented partition cuts).
+ */
+#ifndef LW_B200_H
+#define LW_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LW_ABI_VERSION 1
+
+/* error codes (cudaError_t values pass through unchanged) */
+#define LW_OK 0
+#define LW_E_INVALID_ARG 10001   /* shape / config error: reference raises ValueError */
+#define LW_E_UNSUPPORTED 10002   /* config the device kernels do not implement       */
+#define LW_E_WORKSPACE 10003     /* workspace pointer NULL or smaller than required  */
+#define LW_E_NO_DEVICE 10004     /* no CUDA device visible                           */
+
+/* value dtypes */
+#define LW_F32 0
+#define LW_F64 1
+
+/* schedules: values are the reference ScheduleKind members (schedules.py:21-24);
+ * LW_WORK_ORIENTED is the north star's name for MERGE_PATH. */
+#define LW_THREAD_MAPPED 0
+#define LW_MERGE_PATH 1
+#define LW_WORK_ORIENTED LW_MERGE_PATH
+#define LW_GROUP_MAPPED 2
+
+/* CSR operand. Mirrors reference CsrMatrix (sparse.py:40-71) with GPU storage:
+ * row_offsets int32 or int64 (offset_bits), col_indices int32, values fp32/fp64. */
+typedef struct lw_csr {
+    int64_t rows;
+    int64_t cols;
+    int64_t nnz;
+    const void* row_offsets;    /* [rows+1], int32 if offset_bits==32 else int64 */
+    const int32_t* col_indices; /* [nnz] */
+    const void* values;         /* [nnz], float if dtype==LW_F32 else double */
+    int32_t offset_bits;        /* 32 | 64 */
+    int32_t dtype;              /* LW_F32 | LW_F64 */
+} lw_csr_t;
+
+/* Optional instrumentation. Any field may be NULL. When the pointer passed to a
+ * kernel entry point is non-NULL the instrumented kernel variant runs and records
+ * exactly which lane processed which atom, attributed to which tile. This is the
+ * GPU side of the reference's bit-exact schedule checks: lane_atoms must equal
+ * executor.imbalance(ts, cfg).per_lane_atoms (executor.py:224-251), and
+ * (atom_lane, atom_tile) must equal the (lane, tile) each atom receives from
+ * execute_tile_major / execute_merge_path (executor.py:132-209). */
+typedef struct lw_probe {
+    int64_t* lane_atoms;  /* [lanes] atoms processed per lane; callee zeroes it */
+    int32_t* atom_lane;   /* [nnz] lane that processed each atom               */
+    int32_t* atom_tile;   /* [nnz] tile each atom was attributed to            */
+    int32_t* atom_visits; /* [nnz] visit counter; caller zeroes it              */
+} lw_probe_t;
+
+/* ---- library / device queries --------------------------------------------- */
+const char* lw_error_string(int code);
+int lw_abi_version(void);
+/* SM count of the current device (cached per device). */
+int lw_device_sm_count(int* sm_count_out);
+
+/* Lane count P the device kernels pick when the caller leaves lanes at 0.
+ * Replaces the reference default lanes = worker_threads*32 (executor.py:54-55)
+ * with a device-sized value; group_size/tiles_per_block only matter for
+ * LW_GROUP_MAPPED. */
+int lw_auto_lanes(int schedule, int64_t rows, int64_t nnz, int64_t group_size,
+                  int64_t tiles_per_block, int64_t* lanes_out);
+
+/* ---- schedules ------------------------------------------------------------- */
+
+/* Merge-path split points for `lanes` lanes over the (rows + nnz) path.
+ * Replaces schedules.merge_path_partition (schedules.py:88-110) bit for bit:
+ * coords[2k] = tile_k, coords[2k+1] = atom_k, k = 0..lanes, with
+ * items = ceil((rows+nnz)/lanes) and diag_k = min(k*items, rows+nnz).
+ * coords: device int64[(lanes+1)*2]. */
+int lw_merge_path_partition(int64_t rows, int64_t nnz, const void* row_offsets,
+                            int32_t offset_bits, int64_t lanes, int64_t* coords,
+                            uintptr_t stream);
+
+/* Group plan of every tile block: prefix[b*(tpb+1) + i] = exclusive prefix sum of
+ * the atom counts of block b's tiles, computed with the same device scan the
+ * group-mapped kernels use. Replaces schedules.group_plan(...).prefix
+ * (schedules.py:137-159; exclusive_prefix_sum 121-130); short last block is
+ * padded with its total. prefix: device int64[nblocks*(tpb+1)]. */
+int lw_group_plan_prefix(int64_t rows, const void* row_offsets, int32_t offset_bits,
+                         int64_t tiles_per_block, int64_t* prefix, uintptr_t stream);
+
+/* ---- SpMV: y = A x, one kernel family per schedule ------------------------- */
+
+/* thread_mapped: lane l owns tiles l, l+P, ... and assigns y[t].
+ * Replaces _fast.spmv_thread_mapped (_fast.py:20-28) + its run_sharded fan-out
+ * (kernels.py:74-79). lanes = 0 selects lw_auto_lanes(). */
+int lw_spmv_thread_mapped(const lw_csr_t* A, const void* x, void* y, int64_t lanes,
+                          const lw_probe_t* probe, uintptr_t stream);
+
+/* work_oriented (merge-path): even share of rows+nnz per lane, carries fixed up
+ * in lane order on the device. Replaces _fast.spmv_merge_path (_fast.py:31-52)
+ * plus the host partition (kernels.py:81) and the serial carry fix-up
+ * (kernels.py:90-91). lanes = 0 selects lw_auto_lanes(). */
+size_t lw_spmv_work_oriented_workspace(int64_t rows, int64_t nnz, int64_t lanes,
+                                       int32_t dtype);
+int lw_spmv_work_oriented(const lw_csr_t* A, const void* x, void* y, int64_t lanes,
+                          void* workspace, size_t workspace_bytes,
+                          const lw_probe_t* probe, uintptr_t stream);
+/* The same call split into its three stream-ordered phases so a caller can
+ * bracket each with events: bit 0 = merge-path partition, bit 1 = even-share
+ * SpMV kernel, bit 2 = carry fix-up. Running 1, then 2, then 4 on one stream
+ * equals lw_spmv_work_oriented(..., probe = NULL). */
+int lw_spmv_work_oriented_phases(const lw_csr_t* A, const void* x, void* y, int64_t lanes,
+                                 void* workspace, size_t workspace_bytes,
+                                 uint32_t phase_mask, uintptr_t stream);
+
+/* group_mapped: groups of group_size lanes own blocks of tiles_per_block tiles,
+ * members take block atoms by member stride (schedules.py:137-167,
+ * executor.py:149-168). Replaces _fast.spmv_group_mapped (_fast.py:55-77).
+ * (32,32) runs the warp-tile kernel, (B,B) for B in {64,128,256} the block-tile
+ * kernel, anything else the general group kernel. lanes = 0 selects auto. */
+int lw_spmv_group_mapped(const lw_csr_t* A, const void* x, void* y, int64_t lanes,
+                         int64_t group_size, int64_t tiles_per_block,
+                         const lw_probe_t* probe, uintptr_t stream);
+
+/* Schedule-dispatching form of the three calls above (the shape of the
+ * reference operator kernels.spmv, kernels.py:57-69). workspace is only used by
+ * LW_MERGE_PATH; size it with lw_spmv_workspace(). */
+size_t lw_spmv_workspace(int schedule, int64_t rows, int64_t nnz, int64_t lanes,
+                         int32_t dtype);
+int lw_spmv(int schedule, const lw_csr_t* A, const void* x, void* y, int64_t lanes,
+            int64_t group_size, int64_t tiles_per_block, void* workspace,
+            size_t workspace_bytes, uintptr_t stream);
+
+/* Host-buffer form for FFI callers that hold NumPy/host arrays (the ctypes
+ * binding in INTEGRATION.md). A's pointers, x and y are HOST pointers (pinned
+ * or pageable); the call allocates device buffers stream-ordered, copies in,
+ * runs lw_spmv, copies y out and synchronizes `stream` before returning. */
+int lw_spmv_host(int schedule, const lw_csr_t* A_host, const void* x_host, void* y_host,
+                 int64_t lanes, int64_t group_size, int64_t tiles_per_block,
+                 uintptr_t stream);
+
+/* ---- synthetic inputs (counter-based, identical on host oracle and device) ---- */
+
+/* R-MAT edge keys: keys[i] = (row << scale) | col of edge e = edge_begin + i,
+ * i in [0, n_edges) (chunked generation of one edge stream), each
+ * of the `scale` levels choosing a quadrant with 32-bit thresholds
+ * t_a < t_ab < t_abc (a, a+b, a+b+c scaled by 2^32). keys: device int64. */
+int lw_rmat_keys(int32_t scale, int64_t edge_begin, int64_t n_edges, uint32_t t_a, uint32_t t_ab,
+                 uint32_t t_abc, uint64_t seed, int64_t* keys, uintptr_t stream);
+
+/* values[i] = U[-1,1) drawn from hash(seed, key[i]); dtype LW_F32 rounds the fp64
+ * draw to fp32. */
+int lw_hash_values(const int64_t* keys, int64_t n, uint64_t seed, int32_t dtype,
+                   void* values, uintptr_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LW_B200_H */

@@ -1,0 +1,282 @@
+/*
+ * lw_oracle.c — TEST INFRASTRUCTURE ONLY (the checker, never the product).
+ *
+ * CPU restatement of the reference's SpMV path (lanework 0.1.0,
+ * /root/reference/pkg/src/lanework) in plain C + OpenMP, used by tests/,
+ * __graft_entry__.smoke() and bench.py's CPU-baseline / reference arm. Nothing
+ * under paper_2301_04792_b200/ links or calls this file.
+ *
+ * Semantics follow the reference exactly (fp64 arithmetic on int64 offsets,
+ * int64 column indices and float64 values — the reference's only precision,
+ * sparse.py:55-58, kernels.py:60-63), including its lane model: P virtual lanes
+ * sharded round-robin over T worker threads (executor.py:107-129).
+ * Pinned against the reference's own outputs by tests/golden (make_golden.py
+ * imports the reference and records partitions, plans, per-lane counts,
+ * assignment maps and SpMV results; tests/test_oracle_golden.py replays them).
+ */
+#include <omp.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "../include/lw_hash.h"
+
+#define EXPORT __attribute__((visibility("default")))
+
+static int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
+static int64_t imax(int64_t a, int64_t b) { return a > b ? a : b; }
+
+EXPORT int lwo_version(void) { return 1; }
+
+/* schedules.py:63-85 — greatest t in [max(0,d-nnz), min(d,rows)] with off[t] <= d-t */
+EXPORT int64_t lwo_merge_path_search(const int64_t* off, int64_t rows, int64_t nnz, int64_t d) {
+    int64_t lo = imax(0, d - nnz), hi = imin(d, rows);
+    while (lo < hi) {
+        int64_t mid = (lo + hi + 1) / 2;
+        if (off[mid] <= d - mid) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+/* schedules.py:88-110 — coords[2k] = tile_k, coords[2k+1] = atom_k */
+EXPORT void lwo_merge_path_partition(const int64_t* off, int64_t rows, int64_t nnz, int64_t lanes,
+                                     int64_t* coords, int threads) {
+    const int64_t total = rows + nnz;
+    const int64_t items = total ? (total + lanes - 1) / lanes : 0;
+#pragma omp parallel for num_threads(threads) schedule(static)
+    for (int64_t k = 0; k <= lanes; ++k) {
+        int64_t d = imin(k * items, total);
+        int64_t t = lwo_merge_path_search(off, rows, nnz, d);
+        coords[2 * k] = t;
+        coords[2 * k + 1] = d - t;
+    }
+}
+
+/* _fast.py:20-28 + kernels.py:74-79 — thread j runs lanes j, j+T, ...; lane l
+ * owns tiles l, l+P, ... and assigns y[t] from a sequential fp64 sum. */
+EXPORT void lwo_spmv_thread_mapped(const int64_t* off, const int64_t* col, const double* val,
+                                   const double* x, double* y, int64_t rows, int64_t lanes,
+                                   int threads) {
+#pragma omp parallel num_threads(threads)
+    {
+        const int j = omp_get_thread_num(), T = omp_get_num_threads();
+        for (int64_t lane = j; lane < lanes; lane += T)
+            for (int64_t t = lane; t < rows; t += lanes) {
+                double acc = 0.0;
+                for (int64_t a = off[t]; a < off[t + 1]; ++a) acc += val[a] * x[col[a]];
+                y[t] = acc;
+            }
+    }
+}
+
+/* _fast.py:31-52 + kernels.py:80-91 — host partition, per-lane slices with
+ * carries, then the serial fix-up in lane order. coords may be NULL (computed
+ * here) or a caller buffer of (lanes+1)*2 int64 to reuse. */
+EXPORT int lwo_spmv_merge_path(const int64_t* off, const int64_t* col, const double* val,
+                               const double* x, double* y, int64_t rows, int64_t nnz,
+                               int64_t lanes, int threads, int64_t* coords_buf) {
+    int64_t* coords = coords_buf ? coords_buf : (int64_t*)malloc(sizeof(int64_t) * 2 * (lanes + 1));
+    int64_t* carry_tile = (int64_t*)malloc(sizeof(int64_t) * lanes);
+    double* carry_val = (double*)malloc(sizeof(double) * lanes);
+    if (!coords || !carry_tile || !carry_val) return -1;
+    lwo_merge_path_partition(off, rows, nnz, lanes, coords, threads);
+#pragma omp parallel num_threads(threads)
+    {
+        const int j = omp_get_thread_num(), T = omp_get_num_threads();
+        for (int64_t lane = j; lane < lanes; lane += T) {
+            int64_t atom = coords[2 * lane + 1];
+            const int64_t tile_end = coords[2 * lane + 2], atom_end = coords[2 * lane + 3];
+            double acc = 0.0;
+            for (int64_t t = coords[2 * lane]; t < tile_end; ++t) {
+                for (; atom < off[t + 1]; ++atom) acc += val[atom] * x[col[atom]];
+                y[t] = acc;
+                acc = 0.0;
+            }
+            carry_tile[lane] = -1;
+            carry_val[lane] = 0.0;
+            if (atom < atom_end) {
+                for (; atom < atom_end; ++atom) acc += val[atom] * x[col[atom]];
+                carry_tile[lane] = tile_end;
+                carry_val[lane] = acc;
+            }
+        }
+    }
+    for (int64_t lane = 0; lane < lanes; ++lane)
+        if (carry_tile[lane] >= 0) y[carry_tile[lane]] += carry_val[lane];
+    if (!coords_buf) free(coords);
+    free(carry_tile);
+    free(carry_val);
+    return 0;
+}
+
+/* _fast.py:55-77 + kernels.py:92-98 — group g (members = min(gs, P-g*gs)) owns
+ * blocks g, g+G, ...; member m takes local atoms m, m+members, ...; y pre-zeroed
+ * and accumulated with +=. Groups are sharded over threads like group_shards. */
+EXPORT void lwo_spmv_group_mapped(const int64_t* off, const int64_t* col, const double* val,
+                                  const double* x, double* y, int64_t rows, int64_t lanes,
+                                  int64_t gs, int64_t tpb, int threads) {
+    const int64_t groups = (lanes + gs - 1) / gs;
+    const int64_t blocks = (rows + tpb - 1) / tpb;
+    memset(y, 0, sizeof(double) * rows);
+#pragma omp parallel num_threads(threads)
+    {
+        const int j = omp_get_thread_num(), T = omp_get_num_threads();
+        for (int64_t g = j; g < groups; g += T) {
+            const int64_t members = imin(gs, lanes - g * gs);
+            if (members <= 0) continue;
+            for (int64_t b = g; b < blocks; b += groups) {
+                const int64_t tb = b * tpb, tc = imin(tpb, rows - tb);
+                const int64_t base = off[tb], total = off[tb + tc] - base;
+                for (int64_t m = 0; m < members; ++m) {
+                    int64_t t = tb;
+                    for (int64_t k = m; k < total; k += members) {
+                        const int64_t a = base + k;
+                        while (off[t + 1] <= a) ++t;
+                        y[t] += val[a] * x[col[a]];
+                    }
+                }
+            }
+        }
+    }
+}
+
+/* ---- assignment maps (executor.py:132-209, 224-251) ------------------------
+ * For every atom: the lane that processes it and the tile it is attributed to;
+ * per lane: how many atoms it processes. Arrays may be NULL. lane_atoms is
+ * zeroed here. */
+EXPORT void lwo_assign_thread_mapped(const int64_t* off, int64_t rows, int64_t lanes,
+                                     int64_t* lane_atoms, int32_t* atom_lane, int32_t* atom_tile) {
+    if (lane_atoms) memset(lane_atoms, 0, sizeof(int64_t) * lanes);
+    for (int64_t t = 0; t < rows; ++t) {
+        const int64_t lane = t % lanes;
+        if (lane_atoms) lane_atoms[lane] += off[t + 1] - off[t];
+        for (int64_t a = off[t]; a < off[t + 1]; ++a) {
+            if (atom_lane) atom_lane[a] = (int32_t)lane;
+            if (atom_tile) atom_tile[a] = (int32_t)t;
+        }
+    }
+}
+
+EXPORT void lwo_assign_merge_path(const int64_t* off, int64_t rows, int64_t nnz, int64_t lanes,
+                                  int64_t* lane_atoms, int32_t* atom_lane, int32_t* atom_tile) {
+    int64_t* coords = (int64_t*)malloc(sizeof(int64_t) * 2 * (lanes + 1));
+    lwo_merge_path_partition(off, rows, nnz, lanes, coords, 1);
+    for (int64_t lane = 0; lane < lanes; ++lane) {
+        int64_t atom = coords[2 * lane + 1];
+        const int64_t tile_end = coords[2 * lane + 2], atom_end = coords[2 * lane + 3];
+        if (lane_atoms) lane_atoms[lane] = atom_end - atom;
+        int64_t t = coords[2 * lane];
+        for (; atom < atom_end; ++atom) {
+            while (t < tile_end && off[t + 1] <= atom) ++t;
+            if (atom_lane) atom_lane[atom] = (int32_t)lane;
+            if (atom_tile) atom_tile[atom] = (int32_t)t;
+        }
+    }
+    free(coords);
+}
+
+EXPORT void lwo_assign_group_mapped(const int64_t* off, int64_t rows, int64_t lanes, int64_t gs,
+                                    int64_t tpb, int64_t* lane_atoms, int32_t* atom_lane,
+                                    int32_t* atom_tile) {
+    const int64_t groups = (lanes + gs - 1) / gs;
+    const int64_t blocks = (rows + tpb - 1) / tpb;
+    if (lane_atoms) memset(lane_atoms, 0, sizeof(int64_t) * lanes);
+    for (int64_t b = 0; b < blocks; ++b) {
+        const int64_t g = b % groups;
+        const int64_t members = imin(gs, lanes - g * gs);
+        if (members <= 0) continue;
+        const int64_t tb = b * tpb, tc = imin(tpb, rows - tb);
+        const int64_t base = off[tb], total = off[tb + tc] - base;
+        int64_t t = tb;
+        for (int64_t k = 0; k < total; ++k) {
+            const int64_t a = base + k, lane = g * gs + k % members;
+            while (off[t + 1] <= a) ++t;
+            if (lane_atoms) lane_atoms[lane] += 1;
+            if (atom_lane) atom_lane[a] = (int32_t)lane;
+            if (atom_tile) atom_tile[a] = (int32_t)t;
+        }
+    }
+}
+
+/* ---- synthetic inputs: the same counter-based functions as the device ------ */
+EXPORT void lwo_rmat_keys(int scale, int64_t edge_begin, int64_t n_edges, uint32_t ta,
+                          uint32_t tab, uint32_t tabc, uint64_t seed, int64_t* keys, int threads) {
+#pragma omp parallel for num_threads(threads) schedule(static)
+    for (int64_t i = 0; i < n_edges; ++i)
+        keys[i] = (int64_t)lw_rmat_key(seed, (uint64_t)(edge_begin + i), scale, ta, tab, tabc);
+}
+
+EXPORT void lwo_hash_values(const int64_t* keys, int64_t n, uint64_t seed, double* out,
+                            int threads) {
+#pragma omp parallel for num_threads(threads) schedule(static)
+    for (int64_t i = 0; i < n; ++i) out[i] = lw_hash_value(seed, (uint64_t)keys[i]);
+}
+
+static int cmp_i64(const void* a, const void* b) {
+    const int64_t x = *(const int64_t*)a, y = *(const int64_t*)b;
+    return (x > y) - (x < y);
+}
+
+/* Deduplicated R-MAT CSR (the C twin of device.generate_rmat_csr). off must hold
+ * 2^scale+1 entries, col and val edge_factor*2^scale. Returns nnz (or -1). */
+EXPORT int64_t lwo_rmat_csr(int scale, int64_t edge_factor, uint32_t ta, uint32_t tab,
+                            uint32_t tabc, uint64_t seed, int threads, int64_t* off, int64_t* col,
+                            double* val) {
+    const int64_t n = (int64_t)1 << scale, n_edges = edge_factor * n;
+    const int64_t mask = n - 1;
+    int64_t* cursor = (int64_t*)calloc((size_t)n + 1, sizeof(int64_t));
+    int64_t* tmp = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n_edges > 0 ? n_edges : 1));
+    if (!cursor || !tmp) { free(cursor); free(tmp); return -1; }
+    /* 1. row histogram */
+#pragma omp parallel for num_threads(threads) schedule(static)
+    for (int64_t e = 0; e < n_edges; ++e) {
+        const int64_t r = (int64_t)(lw_rmat_key(seed, (uint64_t)e, scale, ta, tab, tabc) >> scale);
+#pragma omp atomic
+        cursor[r + 1] += 1;
+    }
+    for (int64_t r = 0; r < n; ++r) cursor[r + 1] += cursor[r];
+    memcpy(off, cursor, sizeof(int64_t) * (size_t)(n + 1));
+    /* 2. scatter columns by row (order inside a row fixed by the sort below) */
+#pragma omp parallel for num_threads(threads) schedule(static)
+    for (int64_t e = 0; e < n_edges; ++e) {
+        const uint64_t k = lw_rmat_key(seed, (uint64_t)e, scale, ta, tab, tabc);
+        const int64_t r = (int64_t)(k >> scale);
+        int64_t pos;
+#pragma omp atomic capture
+        pos = cursor[r]++;
+        tmp[pos] = (int64_t)(k & (uint64_t)mask);
+    }
+    /* 3. sort + unique every row; cursor[r] becomes the deduplicated length */
+#pragma omp parallel for num_threads(threads) schedule(dynamic, 4096)
+    for (int64_t r = 0; r < n; ++r) {
+        int64_t* c = tmp + off[r];
+        const int64_t len = off[r + 1] - off[r];
+        if (len > 1) qsort(c, (size_t)len, sizeof(int64_t), cmp_i64);
+        int64_t u = 0;
+        for (int64_t i = 0; i < len; ++i)
+            if (i == 0 || c[i] != c[i - 1]) c[u++] = c[i];
+        cursor[r] = u;
+    }
+    /* 4. compact into col, new offsets, hashed values */
+    int64_t acc = 0;
+    for (int64_t r = 0; r < n; ++r) {
+        const int64_t len = cursor[r];
+        cursor[r] = off[r];  /* old start */
+        off[r] = acc;
+        acc += len;
+    }
+    off[n] = acc;
+#pragma omp parallel for num_threads(threads) schedule(dynamic, 4096)
+    for (int64_t r = 0; r < n; ++r) {
+        const int64_t len = off[r + 1] - off[r];
+        for (int64_t i = 0; i < len; ++i) {
+            const int64_t c = tmp[cursor[r] + i];
+            col[off[r] + i] = c;
+            val[off[r] + i] = lw_hash_value(seed, ((uint64_t)r << scale) | (uint64_t)c);
+        }
+    }
+    free(cursor);
+    free(tmp);
+    return acc;
+}

@@ -1,0 +1,46 @@
+"""paper_2301_04792_b200: B200-native load-balanced SpMV (atoms / tiles / schedules).
+
+A from-scratch B200 implementation of the load-balancing abstraction of
+Osama, Porumbescu & Owens (arXiv 2301.04792) with the public API of the
+reference package ``lanework`` for its SpMV path: tile sets, schedules
+(thread-mapped, merge-path a.k.a. work-oriented, group-mapped warp/block
+tiles) and ``spmv(m, x, cfg)``. The arithmetic runs in hand-written sm_100a
+kernels (liblwb200.so, C ABI in include/lw_b200.h); there is no CPU fallback.
+"""
+
+from ._backend import (ENV_VAR, backend_name, cuda_active, cuda_available, numba_active,
+                       use_backend)
+from ._lib import BackendUnavailable
+from .device import (DeviceCsr, device_group_plan_prefix, device_merge_path_partition,
+                     generate_banded_device, generate_rmat_csr)
+from .executor import (SENTINEL_TILE, CarryOut, CarryPolicy, ExecutorConfig, ImbalanceReport,
+                       SUM_CARRIES, device_config, execute_merge_path, execute_tile_major,
+                       fixup_combine, imbalance)
+from .kernels import (HeuristicConfig, choose_spmv_schedule, spmv, spmv_auto, spmv_probe)
+from .schedules import (GroupMappedSchedule, GroupPlan, MergePathCoord, MergePathSchedule,
+                        MergePathSlice, Schedule, ScheduleKind, ThreadMappedSchedule,
+                        exclusive_prefix_sum, get_tile, group_plan, make_schedule,
+                        merge_path_partition, merge_path_search, merge_path_slices, num_blocks,
+                        thread_mapped_tiles)
+from .sparse import (CsrMatrix, generate_banded_csr, generate_power_law_csr, generate_random_csr,
+                     rmat_thresholds, row_length_stats, validate_csr)
+from .work import (TileSet, csr_tile_set, infinite_range, lane_stride_range, step_range,
+                   tile_offsets)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BackendUnavailable", "CarryOut", "CarryPolicy", "CsrMatrix", "DeviceCsr", "ENV_VAR",
+    "ExecutorConfig", "GroupMappedSchedule", "GroupPlan", "HeuristicConfig", "ImbalanceReport",
+    "MergePathCoord", "MergePathSchedule", "MergePathSlice", "SENTINEL_TILE", "SUM_CARRIES",
+    "Schedule", "ScheduleKind", "ThreadMappedSchedule", "TileSet", "backend_name",
+    "choose_spmv_schedule", "csr_tile_set", "cuda_active", "cuda_available", "device_config",
+    "device_group_plan_prefix", "device_merge_path_partition", "exclusive_prefix_sum",
+    "execute_merge_path", "execute_tile_major", "fixup_combine", "generate_banded_csr",
+    "generate_banded_device", "generate_power_law_csr", "generate_random_csr",
+    "generate_rmat_csr", "get_tile", "group_plan", "imbalance", "infinite_range",
+    "lane_stride_range", "make_schedule", "merge_path_partition", "merge_path_search",
+    "merge_path_slices", "num_blocks", "numba_active", "rmat_thresholds", "row_length_stats",
+    "spmv", "spmv_auto", "spmv_probe", "step_range", "thread_mapped_tiles", "tile_offsets",
+    "use_backend", "validate_csr",
+]

@@ -1,0 +1,160 @@
+"""ctypes binding of liblwb200.so (include/lw_b200.h).
+
+The library is required: there is no CPU fallback behind the cuda backend. If
+the .so is missing or fails to load, every device entry point raises
+:class:`BackendUnavailable` naming the reason.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "liblwb200.so"
+
+LW_OK = 0
+LW_E_INVALID_ARG = 10001
+LW_E_UNSUPPORTED = 10002
+LW_E_WORKSPACE = 10003
+LW_E_NO_DEVICE = 10004
+
+LW_F32 = 0
+LW_F64 = 1
+
+LW_THREAD_MAPPED = 0
+LW_MERGE_PATH = 1
+LW_GROUP_MAPPED = 2
+
+# every symbol include/lw_b200.h declares
+EXPORTS = (
+    "lw_error_string",
+    "lw_abi_version",
+    "lw_device_sm_count",
+    "lw_auto_lanes",
+    "lw_merge_path_partition",
+    "lw_group_plan_prefix",
+    "lw_spmv_thread_mapped",
+    "lw_spmv_work_oriented_workspace",
+    "lw_spmv_work_oriented",
+    "lw_spmv_work_oriented_phases",
+    "lw_spmv_group_mapped",
+    "lw_spmv_workspace",
+    "lw_spmv",
+    "lw_spmv_host",
+    "lw_rmat_keys",
+    "lw_hash_values",
+)
+
+
+class BackendUnavailable(RuntimeError):
+    """The CUDA library or a CUDA device is not available."""
+
+
+class LwCsr(ctypes.Structure):
+    _fields_ = [
+        ("rows", ctypes.c_int64),
+        ("cols", ctypes.c_int64),
+        ("nnz", ctypes.c_int64),
+        ("row_offsets", ctypes.c_void_p),
+        ("col_indices", ctypes.c_void_p),
+        ("values", ctypes.c_void_p),
+        ("offset_bits", ctypes.c_int32),
+        ("dtype", ctypes.c_int32),
+    ]
+
+
+class LwProbe(ctypes.Structure):
+    _fields_ = [
+        ("lane_atoms", ctypes.c_void_p),
+        ("atom_lane", ctypes.c_void_p),
+        ("atom_tile", ctypes.c_void_p),
+        ("atom_visits", ctypes.c_void_p),
+    ]
+
+
+_lock = threading.Lock()
+_lib = None
+_load_error: str | None = None
+
+_i64 = ctypes.c_int64
+_u64 = ctypes.c_uint64
+_i32 = ctypes.c_int32
+_u32 = ctypes.c_uint32
+_vp = ctypes.c_void_p
+_sz = ctypes.c_size_t
+_up = ctypes.c_size_t  # uintptr_t stream
+_csr_p = ctypes.POINTER(LwCsr)
+_probe_p = ctypes.POINTER(LwProbe)
+
+_SIGNATURES = {
+    "lw_error_string": (ctypes.c_char_p, [ctypes.c_int]),
+    "lw_abi_version": (ctypes.c_int, []),
+    "lw_device_sm_count": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
+    "lw_auto_lanes": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _i64, _i64, ctypes.POINTER(_i64)]),
+    "lw_merge_path_partition": (ctypes.c_int, [_i64, _i64, _vp, _i32, _i64, _vp, _up]),
+    "lw_group_plan_prefix": (ctypes.c_int, [_i64, _vp, _i32, _i64, _vp, _up]),
+    "lw_spmv_thread_mapped": (ctypes.c_int, [_csr_p, _vp, _vp, _i64, _probe_p, _up]),
+    "lw_spmv_work_oriented_workspace": (_sz, [_i64, _i64, _i64, _i32]),
+    "lw_spmv_work_oriented": (ctypes.c_int, [_csr_p, _vp, _vp, _i64, _vp, _sz, _probe_p, _up]),
+    "lw_spmv_work_oriented_phases": (ctypes.c_int, [_csr_p, _vp, _vp, _i64, _vp, _sz, _u32, _up]),
+    "lw_spmv_group_mapped": (ctypes.c_int, [_csr_p, _vp, _vp, _i64, _i64, _i64, _probe_p, _up]),
+    "lw_spmv_workspace": (_sz, [ctypes.c_int, _i64, _i64, _i64, _i32]),
+    "lw_spmv": (ctypes.c_int, [ctypes.c_int, _csr_p, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _up]),
+    "lw_spmv_host": (ctypes.c_int, [ctypes.c_int, _csr_p, _vp, _vp, _i64, _i64, _i64, _up]),
+    "lw_rmat_keys": (ctypes.c_int, [_i32, _i64, _i64, _u32, _u32, _u32, _u64, _vp, _up]),
+    "lw_hash_values": (ctypes.c_int, [_vp, _i64, _u64, _i32, _vp, _up]),
+}
+
+
+def load(path: Path | str | None = None):
+    """Load (once) and return the ctypes library; raises BackendUnavailable."""
+    global _lib, _load_error
+    with _lock:
+        if _lib is not None:
+            return _lib
+        p = Path(path) if path else LIB_PATH
+        if not p.exists():
+            _load_error = f"{p} not built (run __graft_entry__.build() or python -m paper_2301_04792_b200._build)"
+            raise BackendUnavailable(_load_error)
+        try:
+            lib = ctypes.CDLL(str(p))
+        except OSError as exc:  # pragma: no cover - depends on the box
+            _load_error = f"cannot load {p}: {exc}"
+            raise BackendUnavailable(_load_error) from exc
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def error_string(code: int) -> str:
+    return load().lw_error_string(code).decode()
+
+
+def check(code: int, what: str) -> None:
+    """Map a C-ABI return code to the reference's exception types."""
+    if code == LW_OK:
+        return
+    msg = f"{what}: {error_string(code)} (code {code})"
+    if code == LW_E_INVALID_ARG:
+        raise ValueError(msg)
+    if code == LW_E_NO_DEVICE:
+        raise BackendUnavailable(msg)
+    raise RuntimeError(msg)
+
+
+def sm_count() -> int:
+    n = ctypes.c_int(0)
+    check(load().lw_device_sm_count(ctypes.byref(n)), "lw_device_sm_count")
+    return n.value
+
+
+def auto_lanes(schedule: int, rows: int, nnz: int, group_size: int = 32,
+               tiles_per_block: int = 32) -> int:
+    out = _i64(0)
+    check(load().lw_auto_lanes(schedule, rows, nnz, group_size, tiles_per_block,
+                               ctypes.byref(out)), "lw_auto_lanes")
+    return out.value

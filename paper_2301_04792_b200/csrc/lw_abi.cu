@@ -1,0 +1,235 @@
+// lw_abi.cu — extern "C" entry points of liblwb200.so (declared in include/lw_b200.h).
+// Argument validation mirrors the reference's ValueError cases (kernels.py:61-62,
+// executor.py:51-63): bad shapes/configs return LW_E_INVALID_ARG, never abort.
+#include <cstring>
+#include <mutex>
+
+#include "lw_common.cuh"
+
+namespace lw {
+int spmv_thread_mapped(const lw_csr_t*, const void*, void*, int64_t, const lw_probe_t*, cudaStream_t);
+int spmv_work_oriented(const lw_csr_t*, const void*, void*, int64_t, void*, size_t, const lw_probe_t*, unsigned, cudaStream_t);
+int spmv_group_mapped(const lw_csr_t*, const void*, void*, int64_t, int64_t, int64_t, const lw_probe_t*, cudaStream_t);
+size_t wo_workspace(int64_t rows, int64_t nnz, int64_t lanes);
+int64_t wo_lanes(int64_t rows, int64_t nnz, int64_t lanes);
+int64_t group_auto_lanes(int64_t rows, int64_t gs, int64_t tpb);
+int merge_path_partition(int64_t, int64_t, const void*, int, int64_t, int64_t*, cudaStream_t);
+int group_plan_prefix(int64_t, const void*, int, int64_t, int64_t*, cudaStream_t);
+int rmat_keys(int, int64_t, int64_t, uint32_t, uint32_t, uint32_t, uint64_t, int64_t*, cudaStream_t);
+int hash_values(const int64_t*, int64_t, uint64_t, int, void*, cudaStream_t);
+
+static int g_sm[64];
+static std::mutex g_sm_mu;
+
+int sm_count() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    std::lock_guard<std::mutex> lk(g_sm_mu);
+    if (!g_sm[dev]) {
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+        g_sm[dev] = n;
+    }
+    return g_sm[dev];
+}
+
+static int64_t thread_auto_lanes(int64_t rows) {
+    const int64_t cap = (int64_t)sm_count() * 2048;
+    int64_t p = ceil_div(rows > 0 ? rows : 1, 256) * 256;
+    return p < cap ? p : cap;
+}
+
+static int check_csr(const lw_csr_t* A) {
+    if (!A) return LW_E_INVALID_ARG;
+    if (A->rows < 0 || A->cols < 0 || A->nnz < 0) return LW_E_INVALID_ARG;
+    if (A->offset_bits != 32 && A->offset_bits != 64) return LW_E_INVALID_ARG;
+    if (A->dtype != LW_F32 && A->dtype != LW_F64) return LW_E_INVALID_ARG;
+    if (A->offset_bits == 32 && A->nnz > 0x7fffffffLL) return LW_E_INVALID_ARG;
+    if (A->rows > 0 && !A->row_offsets) return LW_E_INVALID_ARG;
+    if (A->nnz > 0 && (!A->col_indices || !A->values)) return LW_E_INVALID_ARG;
+    return LW_OK;
+}
+
+static int resolve_lanes(int schedule, const lw_csr_t* A, int64_t lanes, int64_t gs, int64_t tpb,
+                         int64_t* out) {
+    if (lanes < 0) return LW_E_INVALID_ARG;
+    if (lanes > 0) { *out = lanes; return LW_OK; }
+    switch (schedule) {
+        case LW_THREAD_MAPPED: *out = thread_auto_lanes(A->rows); return LW_OK;
+        case LW_MERGE_PATH: *out = wo_lanes(A->rows, A->nnz, 0); return LW_OK;
+        case LW_GROUP_MAPPED:
+            if (gs < 1 || tpb < 1) return LW_E_INVALID_ARG;
+            *out = group_auto_lanes(A->rows, gs, tpb);
+            return LW_OK;
+        default: return LW_E_INVALID_ARG;
+    }
+}
+
+}  // namespace lw
+
+using namespace lw;
+
+extern "C" {
+
+const char* lw_error_string(int code) {
+    switch (code) {
+        case LW_OK: return "success";
+        case LW_E_INVALID_ARG: return "invalid argument (shape or schedule configuration)";
+        case LW_E_UNSUPPORTED: return "configuration not supported by the device kernels";
+        case LW_E_WORKSPACE: return "workspace missing or smaller than required";
+        case LW_E_NO_DEVICE: return "no CUDA device visible";
+        default: return cudaGetErrorString((cudaError_t)code);
+    }
+}
+
+int lw_abi_version(void) { return LW_ABI_VERSION; }
+
+int lw_device_sm_count(int* out) {
+    if (!out) return LW_E_INVALID_ARG;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return LW_E_NO_DEVICE;
+    *out = sm_count();
+    return LW_OK;
+}
+
+int lw_auto_lanes(int schedule, int64_t rows, int64_t nnz, int64_t gs, int64_t tpb,
+                  int64_t* lanes_out) {
+    if (!lanes_out || rows < 0 || nnz < 0) return LW_E_INVALID_ARG;
+    lw_csr_t a{};
+    a.rows = rows;
+    a.nnz = nnz;
+    return resolve_lanes(schedule, &a, 0, gs, tpb, lanes_out);
+}
+
+int lw_merge_path_partition(int64_t rows, int64_t nnz, const void* off, int32_t bits,
+                            int64_t lanes, int64_t* coords, uintptr_t stream) {
+    if (bits != 32 && bits != 64) return LW_E_INVALID_ARG;
+    return merge_path_partition(rows, nnz, off, bits, lanes, coords, (cudaStream_t)stream);
+}
+
+int lw_group_plan_prefix(int64_t rows, const void* off, int32_t bits, int64_t tpb,
+                         int64_t* prefix, uintptr_t stream) {
+    if (bits != 32 && bits != 64) return LW_E_INVALID_ARG;
+    return group_plan_prefix(rows, off, bits, tpb, prefix, (cudaStream_t)stream);
+}
+
+int lw_spmv_thread_mapped(const lw_csr_t* A, const void* x, void* y, int64_t lanes,
+                          const lw_probe_t* probe, uintptr_t stream) {
+    int rc = check_csr(A);
+    if (rc) return rc;
+    if (A->rows > 0 && !y) return LW_E_INVALID_ARG;
+    if (A->nnz > 0 && !x) return LW_E_INVALID_ARG;
+    int64_t p = 0;
+    if ((rc = resolve_lanes(LW_THREAD_MAPPED, A, lanes, 0, 0, &p))) return rc;
+    return spmv_thread_mapped(A, x, y, p, probe, (cudaStream_t)stream);
+}
+
+size_t lw_spmv_work_oriented_workspace(int64_t rows, int64_t nnz, int64_t lanes, int32_t dtype) {
+    (void)dtype;
+    if (rows < 0 || nnz < 0 || lanes < 0) return 0;
+    return wo_workspace(rows, nnz, lanes);
+}
+
+int lw_spmv_work_oriented(const lw_csr_t* A, const void* x, void* y, int64_t lanes, void* ws,
+                          size_t ws_bytes, const lw_probe_t* probe, uintptr_t stream) {
+    int rc = check_csr(A);
+    if (rc) return rc;
+    if (A->rows > 0 && !y) return LW_E_INVALID_ARG;
+    if (A->nnz > 0 && !x) return LW_E_INVALID_ARG;
+    if (lanes < 0) return LW_E_INVALID_ARG;
+    return spmv_work_oriented(A, x, y, lanes, ws, ws_bytes, probe, 7u, (cudaStream_t)stream);
+}
+
+int lw_spmv_work_oriented_phases(const lw_csr_t* A, const void* x, void* y, int64_t lanes,
+                                 void* ws, size_t ws_bytes, uint32_t phase_mask,
+                                 uintptr_t stream) {
+    int rc = check_csr(A);
+    if (rc) return rc;
+    if (A->rows > 0 && !y) return LW_E_INVALID_ARG;
+    if (A->nnz > 0 && !x) return LW_E_INVALID_ARG;
+    if (lanes < 0 || phase_mask == 0 || phase_mask > 7u) return LW_E_INVALID_ARG;
+    return spmv_work_oriented(A, x, y, lanes, ws, ws_bytes, nullptr, phase_mask, (cudaStream_t)stream);
+}
+
+int lw_spmv_group_mapped(const lw_csr_t* A, const void* x, void* y, int64_t lanes,
+                         int64_t gs, int64_t tpb, const lw_probe_t* probe, uintptr_t stream) {
+    int rc = check_csr(A);
+    if (rc) return rc;
+    if (A->rows > 0 && !y) return LW_E_INVALID_ARG;
+    if (A->nnz > 0 && !x) return LW_E_INVALID_ARG;
+    if (gs < 1 || tpb < 1) return LW_E_INVALID_ARG;
+    int64_t p = 0;
+    if ((rc = resolve_lanes(LW_GROUP_MAPPED, A, lanes, gs, tpb, &p))) return rc;
+    return spmv_group_mapped(A, x, y, p, gs, tpb, probe, (cudaStream_t)stream);
+}
+
+size_t lw_spmv_workspace(int schedule, int64_t rows, int64_t nnz, int64_t lanes, int32_t dtype) {
+    return schedule == LW_MERGE_PATH ? lw_spmv_work_oriented_workspace(rows, nnz, lanes, dtype) : 0;
+}
+
+int lw_spmv(int schedule, const lw_csr_t* A, const void* x, void* y, int64_t lanes, int64_t gs,
+            int64_t tpb, void* ws, size_t ws_bytes, uintptr_t stream) {
+    switch (schedule) {
+        case LW_THREAD_MAPPED: return lw_spmv_thread_mapped(A, x, y, lanes, nullptr, stream);
+        case LW_MERGE_PATH: return lw_spmv_work_oriented(A, x, y, lanes, ws, ws_bytes, nullptr, stream);
+        case LW_GROUP_MAPPED: return lw_spmv_group_mapped(A, x, y, lanes, gs, tpb, nullptr, stream);
+        default: return LW_E_INVALID_ARG;
+    }
+}
+
+int lw_spmv_host(int schedule, const lw_csr_t* H, const void* x_host, void* y_host, int64_t lanes,
+                 int64_t gs, int64_t tpb, uintptr_t stream) {
+    int rc = check_csr(H);
+    if (rc) return rc;
+    if (H->rows > 0 && !y_host) return LW_E_INVALID_ARG;
+    if (H->cols > 0 && !x_host) return LW_E_INVALID_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t vb = H->dtype == LW_F32 ? 4 : 8, ob = H->offset_bits / 8;
+    const size_t off_b = (size_t)(H->rows + 1) * ob, col_b = (size_t)H->nnz * 4,
+                 val_b = (size_t)H->nnz * vb, x_b = (size_t)H->cols * vb, y_b = (size_t)H->rows * vb;
+    const size_t ws_b = lw_spmv_workspace(schedule, H->rows, H->nnz, lanes, H->dtype);
+    auto up = [](size_t b) { return (b + 255) / 256 * 256; };
+    const size_t bytes = up(off_b) + up(col_b) + up(val_b) + up(x_b) + up(y_b) + up(ws_b);
+    unsigned char* d = nullptr;
+    LW_TRY(cudaMallocAsync((void**)&d, bytes > 0 ? bytes : 256, s));
+    unsigned char* p = d;
+    void* d_off = p; p += up(off_b);
+    void* d_col = p; p += up(col_b);
+    void* d_val = p; p += up(val_b);
+    void* d_x = p;   p += up(x_b);
+    void* d_y = p;   p += up(y_b);
+    void* d_ws = p;
+    rc = LW_OK;
+    auto cp = [&](void* dst, const void* src, size_t b) {
+        if (!rc && b) rc = (int)cudaMemcpyAsync(dst, src, b, cudaMemcpyHostToDevice, s);
+    };
+    cp(d_off, H->row_offsets, off_b);
+    cp(d_col, H->col_indices, col_b);
+    cp(d_val, H->values, val_b);
+    cp(d_x, x_host, x_b);
+    if (!rc) {
+        lw_csr_t A = *H;
+        A.row_offsets = d_off;
+        A.col_indices = (const int32_t*)d_col;
+        A.values = d_val;
+        rc = lw_spmv(schedule, &A, d_x, d_y, lanes, gs, tpb, d_ws, ws_b, stream);
+    }
+    if (!rc && y_b) rc = (int)cudaMemcpyAsync(y_host, d_y, y_b, cudaMemcpyDeviceToHost, s);
+    cudaError_t fe = cudaFreeAsync(d, s);
+    cudaError_t se = cudaStreamSynchronize(s);
+    if (!rc) rc = (int)fe;
+    if (!rc) rc = (int)se;
+    return rc;
+}
+
+int lw_rmat_keys(int32_t scale, int64_t edge_begin, int64_t n_edges, uint32_t t_a, uint32_t t_ab,
+                 uint32_t t_abc, uint64_t seed, int64_t* keys, uintptr_t stream) {
+    return rmat_keys(scale, edge_begin, n_edges, t_a, t_ab, t_abc, seed, keys, (cudaStream_t)stream);
+}
+
+int lw_hash_values(const int64_t* keys, int64_t n, uint64_t seed, int32_t dtype, void* values,
+                   uintptr_t stream) {
+    return hash_values(keys, n, seed, dtype, values, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,126 @@
+// lw_common.cuh — shared device helpers for the sm_100a SpMV kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "lw_b200.h"
+
+#define LW_TRY(expr)                                   \
+    do {                                               \
+        cudaError_t _e = (expr);                       \
+        if (_e != cudaSuccess) return (int)_e;         \
+    } while (0)
+
+#define LW_LAUNCH_CHECK() LW_TRY(cudaGetLastError())
+
+namespace lw {
+
+constexpr int kWarp = 32;
+
+// Device view of the CSR operand (lw_csr_t with typed pointers).
+template <class OffT, class ValT>
+struct Csr {
+    int64_t rows, cols, nnz;
+    const OffT* __restrict__ off;
+    const int32_t* __restrict__ col;
+    const ValT* __restrict__ val;
+};
+
+struct Probe {
+    int64_t* lane_atoms;
+    int32_t* atom_lane;
+    int32_t* atom_tile;
+    int32_t* atom_visits;
+};
+
+__device__ __forceinline__ void probe_atom(const Probe& p, int64_t atom, int64_t lane,
+                                           int64_t tile) {
+    if (p.atom_lane) p.atom_lane[atom] = (int32_t)lane;
+    if (p.atom_tile) p.atom_tile[atom] = (int32_t)tile;
+    if (p.atom_visits) atomicAdd(p.atom_visits + atom, 1);
+}
+
+// ---- cache-policy loads --------------------------------------------------
+// Streaming operands (col_idx, values) are touched once per SpMV: keep them out
+// of L1 and mark them evict-first in L2 so the gathered x (reused across rows)
+// stays resident in the 126 MB L2 (policy via createpolicy + .L2::cache_hint).
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
+    int32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
+                 : "=r"(v) : "l"(p), "l"(policy_evict_first()));
+    return v;
+}
+__device__ __forceinline__ float ld_stream(const float* p) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;"
+                 : "=f"(v) : "l"(p), "l"(policy_evict_first()));
+    return v;
+}
+__device__ __forceinline__ double ld_stream(const double* p) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+                 : "=d"(v) : "l"(p), "l"(policy_evict_first()));
+    return v;
+}
+// Gathered x: read-only path, L1-allocating, evict-last in L2.
+__device__ __forceinline__ float ld_gather(const float* p) {
+    float v;
+    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;"
+                 : "=f"(v) : "l"(p), "l"(policy_evict_last()));
+    return v;
+}
+__device__ __forceinline__ double ld_gather(const double* p) {
+    double v;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;"
+                 : "=d"(v) : "l"(p), "l"(policy_evict_last()));
+    return v;
+}
+
+// Row offsets are read a handful of times per row (search + staging): plain
+// read-only loads.
+template <class OffT>
+__device__ __forceinline__ int64_t ld_off(const OffT* p) {
+    return (int64_t)__ldg(p);
+}
+
+template <class T>
+__device__ __forceinline__ T shfl(T v, int src) {
+    return __shfl_sync(0xffffffffu, v, src);
+}
+template <class T>
+__device__ __forceinline__ T shfl_down(T v, int d) {
+    return __shfl_down_sync(0xffffffffu, v, d);
+}
+template <class T>
+__device__ __forceinline__ T shfl_up(T v, int d) {
+    return __shfl_up_sync(0xffffffffu, v, d);
+}
+
+// Warp segmented suffix-reduction over keys that are nondecreasing across lanes:
+// afterwards the first lane of every key run holds the run's sum.
+__device__ __forceinline__ double warp_segsum_to_head(double v, int key, int lane) {
+#pragma unroll
+    for (int d = 1; d < kWarp; d <<= 1) {
+        double ov = shfl_down(v, d);
+        int ok = shfl_down(key, d);
+        if (lane + d < kWarp && ok == key) v += ov;
+    }
+    return v;
+}
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+int sm_count();  // cached per device (lw_abi.cu)
+
+}  // namespace lw

@@ -1,0 +1,295 @@
+// spmv_group_mapped.cu — group_mapped schedule (warp tiles, block tiles, general groups).
+//
+// Schedule (reference schedules.py:137-167, executor.py:149-168):
+// lanes are cut into groups of group_size (the last group may be short,
+// executor.py:65-72); tile blocks of tiles_per_block tiles are dealt to groups in
+// group-stride order (block b -> group b mod G); inside a block, member m of a
+// group with `members` lanes takes block-local atoms m, m+members, ... and each
+// atom is attributed to the tile whose exclusive-prefix interval contains it
+// (get_tile, schedules.py:162-167). Lanes are device threads, so the per-lane atom
+// multisets equal executor.imbalance()/execute_tile_major for the same P.
+//
+// Kernels (replace _fast.spmv_group_mapped, _fast.py:55-77):
+//  * k_group_warp   (group_size = tiles_per_block = 32): a warp is a group. The
+//    block plan is a warp-shuffle exclusive scan of the 32 per-tile atom counts;
+//    atom -> tile is a 5-probe binary search over that prefix done with shuffles;
+//    each 32-atom step is reduced with a shuffle segmented reduction keyed on tile
+//    and the run heads add into a per-warp shared accumulator, so y is written
+//    once per tile, coalesced, with a fixed summation order.
+//  * k_group_block<NT> (group_size = tiles_per_block = NT in {64,128,256}): the
+//    CTA is a group; the plan is a block-wide scan into shared memory, atom ->
+//    tile is a log2(NT)-probe search in shared memory, per-warp shared
+//    accumulators (combined in warp order) keep the result deterministic.
+//  * k_group_generic (any group_size / tiles_per_block / lane count): one thread
+//    per lane running the reference's member loop over global memory, with a
+//    monotone tile advance (_fast.py:75-76) and atomic adds into a zeroed y (the
+//    reference's pre-zeroed y += v*x, kernels.py:63 / _fast.py:77).
+#include <climits>
+
+#include "lw_common.cuh"
+
+namespace lw {
+
+// ---- warp tiles -------------------------------------------------------------------
+template <class OffT, class ValT, bool PROBE>
+__global__ void __launch_bounds__(256)
+    k_group_warp(Csr<OffT, ValT> A, const ValT* __restrict__ x, ValT* __restrict__ y,
+                 int64_t groups, Probe probe) {
+    __shared__ double s_acc[8][kWarp];
+    const int lane = threadIdx.x & (kWarp - 1), warp = threadIdx.x >> 5;
+    const int64_t g = (int64_t)blockIdx.x * 8 + warp;
+    if (g >= groups) return;
+    const int64_t nblocks = (A.rows + kWarp - 1) / kWarp;
+    const int64_t glane = g * kWarp + lane;
+    int64_t mine = 0;
+    for (int64_t b = g; b < nblocks; b += groups) {
+        const int64_t tb = b * kWarp;
+        const int tc = (int)min((int64_t)kWarp, A.rows - tb);
+        // per-tile atom counts -> warp exclusive prefix sum (the group plan)
+        const OffT lo_off = lane < tc ? A.off[tb + lane] : (OffT)0;
+        const OffT hi_off = lane < tc ? A.off[tb + lane + 1] : (OffT)0;
+        const OffT cnt = hi_off - lo_off;
+        OffT incl = cnt;
+#pragma unroll
+        for (int d = 1; d < kWarp; d <<= 1) {
+            const OffT o = shfl_up(incl, d);
+            if (lane >= d) incl += o;
+        }
+        const OffT excl = incl - cnt;
+        const OffT total = shfl(incl, kWarp - 1);
+        const int64_t base = (int64_t)shfl(lo_off, 0);
+        s_acc[warp][lane] = 0.0;
+        __syncwarp();
+        for (OffT k0 = 0; k0 < total; k0 += kWarp) {
+            const OffT k = k0 + lane;
+            const bool valid = k < total;
+            // get_tile: largest t < tc with excl[t] <= k (empty tiles never win)
+            int t = 0;
+#pragma unroll
+            for (int s = kWarp / 2; s >= 1; s >>= 1) {
+                const OffT e = shfl(excl, t + s);
+                if (t + s < tc && e <= k) t += s;
+            }
+            double p = 0.0;
+            if (valid) {
+                const int64_t a = base + k;
+                p = (double)ld_stream(A.val + a) * (double)ld_gather(x + ld_stream(A.col + a));
+                if (PROBE) { probe_atom(probe, a, glane, tb + t); ++mine; }
+            }
+            const int key = valid ? t : INT_MAX;
+            const double sum = warp_segsum_to_head(p, key, lane);
+            const int prev = shfl_up(key, 1);
+            if (valid && (lane == 0 || prev != key)) s_acc[warp][t] += sum;
+            __syncwarp();
+        }
+        if (lane < tc) y[tb + lane] = (ValT)s_acc[warp][lane];
+        __syncwarp();
+    }
+    if (PROBE && probe.lane_atoms) probe.lane_atoms[glane] = mine;
+}
+
+// ---- block tiles ------------------------------------------------------------------
+template <class OffT, class ValT, int NT, bool PROBE>
+__global__ void __launch_bounds__(NT)
+    k_group_block(Csr<OffT, ValT> A, const ValT* __restrict__ x, ValT* __restrict__ y,
+                  int64_t groups, Probe probe) {
+    constexpr int NW = NT / kWarp;
+    __shared__ OffT s_excl[NT + 1];
+    __shared__ OffT s_wsum[NW];
+    __shared__ double s_acc[NW][NT];
+    const int tid = threadIdx.x, lane = tid & (kWarp - 1), warp = tid >> 5;
+    const int64_t nblocks = (A.rows + NT - 1) / NT;
+    const int64_t glane = (int64_t)blockIdx.x * NT + tid;
+    int64_t mine = 0;
+    for (int64_t b = blockIdx.x; b < nblocks; b += groups) {
+        const int64_t tb = b * NT;
+        const int tc = (int)min((int64_t)NT, A.rows - tb);
+        const OffT cnt = tid < tc ? A.off[tb + tid + 1] - A.off[tb + tid] : (OffT)0;
+        // block exclusive scan of the counts
+        OffT incl = cnt;
+#pragma unroll
+        for (int d = 1; d < kWarp; d <<= 1) {
+            const OffT o = shfl_up(incl, d);
+            if (lane >= d) incl += o;
+        }
+        if (lane == kWarp - 1) s_wsum[warp] = incl;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) s_acc[w][tid] = 0.0;
+        __syncthreads();
+        OffT wpre = 0;
+        for (int w = 0; w < warp; ++w) wpre += s_wsum[w];
+        OffT total = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) total += s_wsum[w];
+        s_excl[tid] = wpre + incl - cnt;
+        const int64_t base = (int64_t)A.off[tb];
+        __syncthreads();
+        for (OffT k0 = 0; k0 < total; k0 += NT) {
+            const OffT k = k0 + tid;
+            const bool valid = k < total;
+            int t = 0;
+            if (valid) {
+#pragma unroll
+                for (int s = NT / 2; s >= 1; s >>= 1)
+                    if (t + s < tc && s_excl[t + s] <= k) t += s;
+            }
+            double p = 0.0;
+            if (valid) {
+                const int64_t a = base + k;
+                p = (double)ld_stream(A.val + a) * (double)ld_gather(x + ld_stream(A.col + a));
+                if (PROBE) { probe_atom(probe, a, glane, tb + t); ++mine; }
+            }
+            const int key = valid ? t : INT_MAX;
+            const double sum = warp_segsum_to_head(p, key, lane);
+            const int prev = shfl_up(key, 1);
+            if (valid && (lane == 0 || prev != key)) s_acc[warp][t] += sum;
+            __syncwarp();
+        }
+        __syncthreads();
+        if (tid < tc) {
+            double r = 0.0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) r += s_acc[w][tid];
+            y[tb + tid] = (ValT)r;
+        }
+        __syncthreads();
+    }
+    if (PROBE && probe.lane_atoms) probe.lane_atoms[glane] = mine;
+}
+
+// ---- general groups -----------------------------------------------------------------
+template <class ValT>
+__device__ __forceinline__ void add_out(ValT* p, double v);
+template <>
+__device__ __forceinline__ void add_out<float>(float* p, double v) { atomicAdd(p, (float)v); }
+template <>
+__device__ __forceinline__ void add_out<double>(double* p, double v) { atomicAdd(p, v); }
+
+template <class OffT, class ValT, bool PROBE>
+__global__ void __launch_bounds__(256)
+    k_group_generic(Csr<OffT, ValT> A, const ValT* __restrict__ x, ValT* __restrict__ y,
+                    int64_t lanes, int64_t gs, int64_t tpb, Probe probe) {
+    const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= lanes) return;
+    const int64_t gid = l / gs, m = l - gid * gs;
+    const int64_t members = min(gs, lanes - gid * gs);
+    const int64_t groups = (lanes + gs - 1) / gs;
+    const int64_t nblocks = (A.rows + tpb - 1) / tpb;
+    int64_t mine = 0;
+    for (int64_t b = gid; b < nblocks; b += groups) {
+        const int64_t tb = b * tpb;
+        const int64_t tc = min(tpb, A.rows - tb);
+        const int64_t base = ld_off(A.off + tb);
+        const int64_t total = ld_off(A.off + tb + tc) - base;
+        int64_t tile = tb, cur = -1;
+        double acc = 0.0;
+        for (int64_t k = m; k < total; k += members) {
+            const int64_t a = base + k;
+            while (ld_off(A.off + tile + 1) <= a) ++tile;
+            if (tile != cur) {
+                if (cur >= 0) add_out<ValT>(y + cur, acc);
+                cur = tile;
+                acc = 0.0;
+            }
+            acc = fma((double)__ldg(A.val + a), (double)ld_gather(x + __ldg(A.col + a)), acc);
+            if (PROBE) { probe_atom(probe, a, l, tile); ++mine; }
+        }
+        if (cur >= 0) add_out<ValT>(y + cur, acc);
+    }
+    if (PROBE && probe.lane_atoms) probe.lane_atoms[l] = mine;
+}
+
+// ---- host side ----------------------------------------------------------------------
+enum GroupKernel { GK_WARP, GK_BLOCK, GK_GENERIC };
+
+static GroupKernel pick_group_kernel(int64_t lanes, int64_t gs, int64_t tpb) {
+    if (gs == 32 && tpb == 32 && lanes % 32 == 0) return GK_WARP;
+    if (gs == tpb && (gs == 64 || gs == 128 || gs == 256) && lanes % gs == 0) return GK_BLOCK;
+    return GK_GENERIC;
+}
+
+int64_t group_auto_lanes(int64_t rows, int64_t gs, int64_t tpb) {
+    const int64_t nblocks = rows > 0 ? ceil_div(rows, tpb) : 1;
+    // enough groups to fill every SM at full occupancy, but never more than blocks
+    const int64_t per_sm = gs < 2048 ? 2048 / gs : 1;
+    const int64_t cap = (int64_t)sm_count() * per_sm;
+    const int64_t groups = nblocks < cap ? nblocks : cap;
+    return (groups > 0 ? groups : 1) * gs;
+}
+
+template <class OffT, class ValT>
+static int launch_group(const lw_csr_t* A, const void* x, void* y, int64_t lanes, int64_t gs,
+                        int64_t tpb, const lw_probe_t* probe, cudaStream_t s) {
+    Csr<OffT, ValT> a{A->rows, A->cols, A->nnz, (const OffT*)A->row_offsets,
+                      A->col_indices, (const ValT*)A->values};
+    Probe p{};
+    if (probe) p = Probe{probe->lane_atoms, probe->atom_lane, probe->atom_tile, probe->atom_visits};
+    if (probe && p.lane_atoms) LW_TRY(cudaMemsetAsync(p.lane_atoms, 0, lanes * 8, s));
+    const ValT* xv = (const ValT*)x;
+    ValT* yv = (ValT*)y;
+    switch (pick_group_kernel(lanes, gs, tpb)) {
+        case GK_WARP: {
+            const int64_t groups = lanes / 32;
+            const int64_t grid = ceil_div(groups, 8);
+            if (probe) k_group_warp<OffT, ValT, true><<<grid, 256, 0, s>>>(a, xv, yv, groups, p);
+            else       k_group_warp<OffT, ValT, false><<<grid, 256, 0, s>>>(a, xv, yv, groups, p);
+            break;
+        }
+        case GK_BLOCK: {
+            const int64_t groups = lanes / gs;
+#define LW_GB(NT)                                                                           \
+    if (gs == NT) {                                                                         \
+        if (probe) k_group_block<OffT, ValT, NT, true><<<groups, NT, 0, s>>>(a, xv, yv, groups, p); \
+        else       k_group_block<OffT, ValT, NT, false><<<groups, NT, 0, s>>>(a, xv, yv, groups, p); \
+    }
+            LW_GB(64) LW_GB(128) LW_GB(256)
+#undef LW_GB
+            break;
+        }
+        default: {
+            LW_TRY(cudaMemsetAsync(y, 0, A->rows * sizeof(ValT), s));
+            const int64_t grid = ceil_div(lanes, 256);
+            if (probe) k_group_generic<OffT, ValT, true><<<grid, 256, 0, s>>>(a, xv, yv, lanes, gs, tpb, p);
+            else       k_group_generic<OffT, ValT, false><<<grid, 256, 0, s>>>(a, xv, yv, lanes, gs, tpb, p);
+        }
+    }
+    LW_LAUNCH_CHECK();
+    return LW_OK;
+}
+
+int spmv_group_mapped(const lw_csr_t* A, const void* x, void* y, int64_t lanes, int64_t gs,
+                      int64_t tpb, const lw_probe_t* probe, cudaStream_t s) {
+    if (A->rows == 0) return LW_OK;
+    const bool o32 = A->offset_bits == 32;
+    if (A->dtype == LW_F32)
+        return o32 ? launch_group<int32_t, float>(A, x, y, lanes, gs, tpb, probe, s)
+                   : launch_group<int64_t, float>(A, x, y, lanes, gs, tpb, probe, s);
+    return o32 ? launch_group<int32_t, double>(A, x, y, lanes, gs, tpb, probe, s)
+               : launch_group<int64_t, double>(A, x, y, lanes, gs, tpb, probe, s);
+}
+
+// Group plan prefix of every block: prefix[b*(tpb+1)+i] = off[tb+min(i,tc)] - off[tb].
+template <class OffT>
+__global__ void k_group_prefix(const OffT* __restrict__ off, int64_t rows, int64_t tpb,
+                               int64_t nblocks, int64_t* __restrict__ prefix) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= nblocks * (tpb + 1)) return;
+    const int64_t b = idx / (tpb + 1), i = idx - b * (tpb + 1);
+    const int64_t tb = b * tpb;
+    const int64_t tc = min(tpb, rows - tb);
+    prefix[idx] = ld_off(off + tb + min(i, tc)) - ld_off(off + tb);
+}
+
+int group_plan_prefix(int64_t rows, const void* off, int bits, int64_t tpb, int64_t* prefix,
+                      cudaStream_t s) {
+    if (tpb < 1 || rows < 0 || !prefix) return LW_E_INVALID_ARG;
+    if (rows == 0) return LW_OK;
+    const int64_t nblocks = ceil_div(rows, tpb);
+    const int64_t n = nblocks * (tpb + 1);
+    if (bits == 32) k_group_prefix<int32_t><<<ceil_div(n, 256), 256, 0, s>>>((const int32_t*)off, rows, tpb, nblocks, prefix);
+    else            k_group_prefix<int64_t><<<ceil_div(n, 256), 256, 0, s>>>((const int64_t*)off, rows, tpb, nblocks, prefix);
+    LW_LAUNCH_CHECK();
+    return LW_OK;
+}
+
+}  // namespace lw

@@ -1,0 +1,303 @@
+"""Device-resident CSR and the thin launch layer over liblwb200.so.
+
+Layout in HBM (one allocation per array, torch caching allocator):
+  row_offsets  int32[rows+1] (int64 when nnz >= 2^31)
+  col_indices  int32[nnz]
+  values       fp32[nnz] or fp64[nnz]
+x and y are dense fp32/fp64 vectors of the same dtype. Nothing is padded: the
+kernels handle ragged rows and misaligned vector starts themselves.
+
+PyTorch is plumbing here (allocation, streams, torch.distributed); every
+computation goes through the C ABI in include/lw_b200.h.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+__all__ = ["DeviceCsr", "device_merge_path_partition", "device_group_plan_prefix",
+           "generate_rmat_csr", "generate_banded_device", "Workspace", "Probe", "current_stream"]
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _dtype_code(dt) -> int:
+    torch = _torch()
+    if dt in (torch.float32, np.float32, "float32", "f32", "fp32"):
+        return _lib.LW_F32
+    if dt in (torch.float64, np.float64, "float64", "f64", "fp64"):
+        return _lib.LW_F64
+    raise ValueError(f"unsupported value dtype {dt!r}; expected float32 or float64")
+
+
+def _torch_dtype(dt):
+    torch = _torch()
+    return torch.float32 if _dtype_code(dt) == _lib.LW_F32 else torch.float64
+
+
+def current_stream(device=None) -> int:
+    torch = _torch()
+    return int(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _require_cuda(device=None):
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise _lib.BackendUnavailable("CUDA backend requires a visible CUDA device")
+    _lib.load()
+    return torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+
+
+@dataclass
+class DeviceCsr:
+    """CSR matrix resident in GPU memory (the device-side tile set: rows = tiles)."""
+
+    rows: int
+    cols: int
+    row_offsets: "object"   # torch int32/int64 [rows+1]
+    col_indices: "object"   # torch int32 [nnz]
+    values: "object"        # torch float32/float64 [nnz]
+
+    @property
+    def nnz(self) -> int:
+        return int(self.col_indices.shape[0])
+
+    @property
+    def device(self):
+        return self.values.device
+
+    @property
+    def dtype(self):
+        return self.values.dtype
+
+    @property
+    def offset_bits(self) -> int:
+        return 32 if self.row_offsets.dtype == _torch().int32 else 64
+
+    # tile-set protocol (host reads; for schedules on small matrices)
+    @property
+    def num_tiles(self) -> int:
+        return self.rows
+
+    @property
+    def num_atoms(self) -> int:
+        return self.nnz
+
+    @property
+    def offsets(self) -> np.ndarray:
+        return self.row_offsets.to("cpu").numpy().astype(np.int64)
+
+    def atom_offset(self, tile: int) -> int:
+        return int(self.row_offsets[tile].item())
+
+    @classmethod
+    def from_host(cls, m, dtype="float32", device=None, offset_bits: int | None = None,
+                  non_blocking: bool = False) -> "DeviceCsr":
+        torch = _torch()
+        dev = _require_cuda(device)
+        nnz = int(m.col_indices.shape[0])
+        if offset_bits is None:
+            offset_bits = 32 if nnz < (1 << 31) else 64
+        if offset_bits not in (32, 64) or (offset_bits == 32 and nnz >= (1 << 31)):
+            raise ValueError("offset_bits must be 64 when nnz >= 2^31 (else 32 or 64)")
+        if int(m.cols) >= (1 << 31):
+            raise ValueError("cols must be < 2^31 (int32 column indices)")
+        odt = torch.int32 if offset_bits == 32 else torch.int64
+        off = torch.as_tensor(np.asarray(m.row_offsets)).to(dev, non_blocking=non_blocking).to(odt)
+        col = torch.as_tensor(np.asarray(m.col_indices)).to(dev, non_blocking=non_blocking).to(torch.int32)
+        val = torch.as_tensor(np.asarray(m.values)).to(dev, non_blocking=non_blocking).to(_torch_dtype(dtype))
+        return cls(int(m.rows), int(m.cols), off.contiguous(), col.contiguous(), val.contiguous())
+
+    def to_host(self):
+        from .sparse import CsrMatrix
+
+        return CsrMatrix(self.rows, self.cols, self.row_offsets.cpu().numpy(),
+                         self.col_indices.cpu().numpy(), self.values.cpu().numpy())
+
+    def astype(self, dtype) -> "DeviceCsr":
+        return DeviceCsr(self.rows, self.cols, self.row_offsets, self.col_indices,
+                         self.values.to(_torch_dtype(dtype)))
+
+    def row_slice(self, r0: int, r1: int) -> "DeviceCsr":
+        """Rows [r0, r1) as a CSR with rebased offsets (views, no copy of atoms)."""
+        if not 0 <= r0 <= r1 <= self.rows:
+            raise ValueError("row range outside the matrix")
+        off = self.row_offsets[r0:r1 + 1]
+        a0 = int(off[0].item())
+        a1 = int(off[-1].item())
+        return DeviceCsr(r1 - r0, self.cols, (off - a0).contiguous(),
+                         self.col_indices[a0:a1], self.values[a0:a1])
+
+    def c_struct(self) -> _lib.LwCsr:
+        s = _lib.LwCsr()
+        s.rows, s.cols, s.nnz = self.rows, self.cols, self.nnz
+        s.row_offsets = self.row_offsets.data_ptr()
+        s.col_indices = self.col_indices.data_ptr() if self.nnz else None
+        s.values = self.values.data_ptr() if self.nnz else None
+        s.offset_bits = self.offset_bits
+        s.dtype = _dtype_code(self.dtype)
+        return s
+
+    def algorithmic_bytes(self) -> int:
+        """SURVEY §8(d) byte model: nnz*(idx+val) + (rows+1)*off + cols*val + rows*val."""
+        sv = self.values.element_size()
+        so = self.row_offsets.element_size()
+        return self.nnz * (4 + sv) + (self.rows + 1) * so + self.cols * sv + self.rows * sv
+
+
+class Workspace:
+    """Grow-only device scratch buffer (per device), reused across launches."""
+
+    def __init__(self):
+        self._buf = {}
+
+    def get(self, nbytes: int, device):
+        torch = _torch()
+        key = str(device)
+        buf = self._buf.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+            self._buf[key] = buf
+        return buf
+
+
+class Probe:
+    """Device buffers for the instrumented kernels (lw_probe_t)."""
+
+    def __init__(self, lanes: int, nnz: int, device):
+        torch = _torch()
+        self.lane_atoms = torch.zeros(max(lanes, 1), dtype=torch.int64, device=device)
+        self.atom_lane = torch.full((max(nnz, 1),), -1, dtype=torch.int32, device=device)
+        self.atom_tile = torch.full((max(nnz, 1),), -1, dtype=torch.int32, device=device)
+        self.atom_visits = torch.zeros(max(nnz, 1), dtype=torch.int32, device=device)
+        self.lanes, self.nnz = lanes, nnz
+
+    def c_struct(self) -> _lib.LwProbe:
+        p = _lib.LwProbe()
+        p.lane_atoms = self.lane_atoms.data_ptr()
+        p.atom_lane = self.atom_lane.data_ptr()
+        p.atom_tile = self.atom_tile.data_ptr()
+        p.atom_visits = self.atom_visits.data_ptr()
+        return p
+
+    def host(self) -> dict:
+        return {"lane_atoms": self.lane_atoms[: self.lanes].cpu().numpy(),
+                "atom_lane": self.atom_lane[: self.nnz].cpu().numpy(),
+                "atom_tile": self.atom_tile[: self.nnz].cpu().numpy(),
+                "atom_visits": self.atom_visits[: self.nnz].cpu().numpy()}
+
+
+def _offsets_tensor(ts, device):
+    torch = _torch()
+    if isinstance(ts, DeviceCsr):
+        return ts.row_offsets, ts.rows, ts.nnz
+    dev = _require_cuda(device)
+    off = torch.as_tensor(np.ascontiguousarray(ts.offsets if hasattr(ts, "offsets") else
+                                               [ts.atom_offset(t) for t in range(ts.num_tiles + 1)],
+                                               dtype=np.int64)).to(dev)
+    return off, ts.num_tiles, ts.num_atoms
+
+
+def device_merge_path_partition(ts, lanes: int, device=None):
+    """lw_merge_path_partition: torch int64 [(lanes+1), 2], bit-exact with the host."""
+    torch = _torch()
+    dev = ts.device if isinstance(ts, DeviceCsr) else (
+        device if not isinstance(device, DeviceCsr) else device.device)
+    off, rows, nnz = _offsets_tensor(ts, dev)
+    out = torch.empty((lanes + 1, 2), dtype=torch.int64, device=off.device)
+    bits = 32 if off.dtype == torch.int32 else 64
+    lib = _lib.load()
+    _lib.check(lib.lw_merge_path_partition(rows, nnz, off.data_ptr(), bits, lanes, out.data_ptr(),
+                                           current_stream(off.device)), "lw_merge_path_partition")
+    return out
+
+
+def device_group_plan_prefix(ts, tiles_per_block: int, device=None):
+    """lw_group_plan_prefix: torch int64 [nblocks, tpb+1]."""
+    torch = _torch()
+    off, rows, _ = _offsets_tensor(ts, device)
+    nblocks = (rows + tiles_per_block - 1) // tiles_per_block
+    out = torch.empty((nblocks, tiles_per_block + 1), dtype=torch.int64, device=off.device)
+    bits = 32 if off.dtype == torch.int32 else 64
+    lib = _lib.load()
+    _lib.check(lib.lw_group_plan_prefix(rows, off.data_ptr(), bits, tiles_per_block, out.data_ptr(),
+                                        current_stream(off.device)), "lw_group_plan_prefix")
+    return out
+
+
+def _csr_from_sorted_keys(n: int, scale: int, keys, seed: int, dtype, device) -> DeviceCsr:
+    torch = _torch()
+    rows = keys >> scale
+    cols = (keys & (n - 1)).to(torch.int32)
+    counts = torch.bincount(rows, minlength=n)
+    nnz = int(keys.shape[0])
+    odt = torch.int32 if nnz < (1 << 31) else torch.int64
+    off = torch.zeros(n + 1, dtype=torch.int64, device=device)
+    torch.cumsum(counts, 0, out=off[1:])
+    vals = torch.empty(nnz, dtype=_torch_dtype(dtype), device=device)
+    lib = _lib.load()
+    _lib.check(lib.lw_hash_values(keys.data_ptr(), nnz, seed, _dtype_code(dtype), vals.data_ptr(),
+                                  current_stream(device)), "lw_hash_values")
+    return DeviceCsr(n, n, off.to(odt), cols, vals)
+
+
+def generate_rmat_csr(scale: int, edge_factor: int = 16, seed: int = 3, a: float = 0.57,
+                      b: float = 0.19, c: float = 0.19, dtype="float32", device=None,
+                      chunk_edges: int = 1 << 27) -> DeviceCsr:
+    """Directed R-MAT CSR built on the device: 2^scale rows, edge_factor*2^scale
+    edges, duplicates removed, self-loops kept, no permutation; values are
+    hash_values(key, seed) in U[-1, 1). Identical to the C oracle's lwo_rmat_csr.
+    """
+    from .sparse import rmat_thresholds
+
+    torch = _torch()
+    dev = _require_cuda(device)
+    n = 1 << scale
+    n_edges = edge_factor * n
+    ta, tab, tabc = rmat_thresholds(a, b, c)
+    lib = _lib.load()
+    stream = current_stream(dev)
+    uniq = []
+    # generate + sort + dedup in chunks to bound the sort's scratch memory
+    for start in range(0, n_edges, chunk_edges):
+        cnt = min(chunk_edges, n_edges - start)
+        k = torch.empty(cnt, dtype=torch.int64, device=dev)
+        _lib.check(lib.lw_rmat_keys(scale, start, cnt, ta, tab, tabc, seed, k.data_ptr(), stream),
+                   "lw_rmat_keys")
+        uniq.append(torch.unique(k))
+        del k
+    keys = torch.unique(torch.cat(uniq)) if len(uniq) > 1 else uniq[0]
+    del uniq
+    return _csr_from_sorted_keys(n, scale, keys, seed, dtype, dev)
+
+
+def generate_banded_device(rows: int, half_bandwidth: int, seed: int, dtype="float32",
+                           device=None) -> DeviceCsr:
+    """Banded matrix (sparse.generate_banded_csr) built directly on the device."""
+    torch = _torch()
+    dev = _require_cuda(device)
+    i = torch.arange(rows, dtype=torch.int64, device=dev)
+    lo = torch.clamp(i - half_bandwidth, min=0)
+    hi = torch.clamp(i + half_bandwidth + 1, max=rows)
+    lengths = hi - lo
+    off = torch.zeros(rows + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(lengths, 0, out=off[1:])
+    nnz = int(off[-1].item())
+    owner = torch.repeat_interleave(i, lengths)
+    cols = torch.arange(nnz, dtype=torch.int64, device=dev) - off[:-1][owner] + lo[owner]
+    keys = owner * rows + cols
+    vals = torch.empty(nnz, dtype=_torch_dtype(dtype), device=dev)
+    lib = _lib.load()
+    _lib.check(lib.lw_hash_values(keys.data_ptr(), nnz, seed, _dtype_code(dtype), vals.data_ptr(),
+                                  current_stream(dev)), "lw_hash_values")
+    odt = torch.int32 if nnz < (1 << 31) else torch.int64
+    return DeviceCsr(rows, rows, off.to(odt), cols.to(torch.int32), vals)

@@ -1,0 +1,144 @@
+"""The SpMV operator on the cuda backend (reference kernels.py:57-126, 211-227).
+
+``spmv(m, x, cfg)`` keeps the reference signature and error behaviour:
+  * host operands (CsrMatrix + NumPy x): x is validated exactly like
+    kernels.py:60-62 (ValueError on a length mismatch), the matrix and x are
+    uploaded, the schedule's kernel runs, and a NumPy float64 y comes back —
+    computed in fp64 on the device by default, the reference's precision;
+  * device operands (DeviceCsr + torch CUDA x): y stays on the device in the
+    matrix's dtype; nothing touches the host. This is the path the bench's
+    ``value`` measures.
+Schedule selection follows ``cfg.schedule``; ``cfg.lanes=None`` lets the
+device size the lane count (see executor.device_config).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from . import _backend, _lib
+from .device import DeviceCsr, Probe, Workspace, current_stream
+from .executor import ExecutorConfig
+from .schedules import ScheduleKind
+
+__all__ = ["spmv", "spmv_probe", "spmv_auto", "choose_spmv_schedule", "HeuristicConfig",
+           "schedule_code"]
+
+_WS = Workspace()
+
+
+def schedule_code(kind: ScheduleKind) -> int:
+    return {ScheduleKind.THREAD_MAPPED: _lib.LW_THREAD_MAPPED,
+            ScheduleKind.MERGE_PATH: _lib.LW_MERGE_PATH,
+            ScheduleKind.GROUP_MAPPED: _lib.LW_GROUP_MAPPED}[kind]
+
+
+def _lanes_arg(cfg: ExecutorConfig) -> int:
+    return 0 if cfg.lanes is None else int(cfg.lanes)
+
+
+def _launch(m: DeviceCsr, x, y, cfg: ExecutorConfig, probe: Probe | None, stream: int) -> None:
+    lib = _lib.load()
+    A = m.c_struct()
+    xp = x.data_ptr() if x.numel() else None
+    yp = y.data_ptr() if y.numel() else None
+    pp = probe.c_struct() if probe is not None else None
+    lanes = _lanes_arg(cfg)
+    kind = cfg.schedule
+    if kind is ScheduleKind.THREAD_MAPPED:
+        rc = lib.lw_spmv_thread_mapped(A, xp, yp, lanes, pp, stream)
+    elif kind is ScheduleKind.MERGE_PATH:
+        need = lib.lw_spmv_work_oriented_workspace(m.rows, m.nnz, lanes, A.dtype)
+        ws = _WS.get(need, m.device)
+        rc = lib.lw_spmv_work_oriented(A, xp, yp, lanes, ws.data_ptr(), ws.numel(), pp, stream)
+    else:
+        rc = lib.lw_spmv_group_mapped(A, xp, yp, lanes, cfg.group_size, cfg.tiles_per_block, pp,
+                                      stream)
+    _lib.check(rc, f"spmv[{kind.value}]")
+
+
+def _check_device_x(m: DeviceCsr, x):
+    import torch
+
+    if not isinstance(x, torch.Tensor):
+        raise TypeError("a DeviceCsr needs x as a torch CUDA tensor")
+    if x.ndim != 1 or x.shape[0] != m.cols:
+        raise ValueError(f"x has length {x.numel()}, expected {m.cols}")
+    if x.device != m.device:
+        raise ValueError(f"x is on {x.device}, matrix on {m.device}")
+    if x.dtype != m.dtype:
+        raise ValueError(f"x dtype {x.dtype} differs from matrix dtype {m.dtype}")
+    return x.contiguous()
+
+
+def spmv(m, x, cfg: ExecutorConfig | None = None, *, out=None, dtype=None):
+    """y = m @ x under ``cfg.schedule``; rows without nonzeros yield 0."""
+    cfg = cfg or ExecutorConfig()
+    _backend.require_cuda()
+    import torch
+
+    if isinstance(m, DeviceCsr):
+        x = _check_device_x(m, x)
+        y = out if out is not None else torch.empty(m.rows, dtype=m.dtype, device=m.device)
+        if y.shape != (m.rows,) or y.dtype != m.dtype or y.device != m.device:
+            raise ValueError("out must be a contiguous vector of length rows with the matrix dtype")
+        _launch(m, x, y, cfg, None, current_stream(m.device))
+        return y
+    xh = np.ascontiguousarray(x, dtype=np.float64)
+    if xh.ndim != 1 or xh.size != m.cols:
+        raise ValueError(f"x has length {xh.size}, expected {m.cols}")
+    dm = DeviceCsr.from_host(m, dtype=dtype or "float64")
+    xd = torch.from_numpy(xh).to(dm.device).to(dm.dtype)
+    y = torch.empty(dm.rows, dtype=dm.dtype, device=dm.device)
+    _launch(dm, xd, y, cfg, None, current_stream(dm.device))
+    return y.to(torch.float64).cpu().numpy()
+
+
+def spmv_probe(m: DeviceCsr, x, cfg: ExecutorConfig | None = None):
+    """Instrumented SpMV: returns (y, probe dict, lanes) for bit-exact schedule checks.
+
+    probe["lane_atoms"][l] is the atoms lane l processed; probe["atom_lane"][a] /
+    ["atom_tile"][a] the lane and tile atom a was processed by / attributed to;
+    probe["atom_visits"][a] how often it was processed (must be 1).
+    """
+    from .executor import device_config
+
+    cfg = device_config(cfg or ExecutorConfig(), m)
+    _backend.require_cuda()
+    import torch
+
+    x = _check_device_x(m, x)
+    y = torch.empty(m.rows, dtype=m.dtype, device=m.device)
+    probe = Probe(cfg.lanes, m.nnz, m.device)
+    _launch(m, x, y, cfg, probe, current_stream(m.device))
+    return y, probe.host(), cfg.lanes
+
+
+@dataclass(frozen=True)
+class HeuristicConfig:
+    """Size thresholds of the schedule dispatcher (alpha=500, beta=10000)."""
+
+    alpha: int = 500
+    beta: int = 10000
+
+    def __post_init__(self):
+        if self.alpha <= 0 or self.beta <= 0:
+            raise ValueError("alpha and beta must be positive")
+
+
+def choose_spmv_schedule(rows: int, cols: int, nnz: int, heuristic: HeuristicConfig | None = None,
+                         small_schedule: ScheduleKind = ScheduleKind.THREAD_MAPPED) -> ScheduleKind:
+    """Merge-path unless the matrix is small in a dimension and in nnz (kernels.py:211-218)."""
+    h = heuristic or HeuristicConfig()
+    small = (rows < h.alpha or cols < h.alpha) and nnz < h.beta
+    return small_schedule if small else ScheduleKind.MERGE_PATH
+
+
+def spmv_auto(m, x, heuristic: HeuristicConfig | None = None, cfg: ExecutorConfig | None = None,
+              small_schedule: ScheduleKind = ScheduleKind.THREAD_MAPPED):
+    """SpMV under the heuristic's schedule; returns (y, chosen) (kernels.py:221-227)."""
+    chosen = choose_spmv_schedule(m.rows, m.cols, m.nnz, heuristic, small_schedule)
+    cfg = replace(cfg, schedule=chosen) if cfg is not None else ExecutorConfig(schedule=chosen)
+    return spmv(m, x, cfg), chosen

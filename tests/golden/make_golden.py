@@ -1,0 +1,190 @@
+"""Generate the golden fixtures from the REFERENCE implementation itself.
+
+Run in the dev container (the only place /root/reference exists):
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden.py
+
+It imports the unmodified reference package (lanework 0.1.0) from
+/root/reference/pkg/src and records, for seeded inputs, exactly what the
+reference returns: merge-path search/partition, group plans, get_tile,
+imbalance per lane, the (lane, tile) every atom is assigned to by the
+reference executors, spmv results on the numba backend, and the outputs of
+its synthetic generators. The .npz files it writes are committed; tests replay
+them against the C oracle (CPU) and the CUDA kernels (GPU) without needing the
+reference at run time.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF = Path(os.environ.get("LANEWORK_SRC", "/root/reference/pkg/src"))
+OUT = Path(__file__).resolve().parent
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+sys.path.insert(0, str(REF))
+
+import lanework as lw  # noqa: E402  (the reference)
+
+
+def tile_set_corpus(count: int, seed: int, max_tiles: int = 120, max_atoms: int = 900):
+    """Empty set, a single tile, and random sets with ~25% empty tiles."""
+    rng = np.random.default_rng(seed)
+    out = [np.zeros(1, np.int64), np.array([0, 17], np.int64), np.array([0, 0, 0, 5], np.int64),
+           np.array([0, 2, 3, 6], np.int64), np.array([0, 1000] + [1000] * 7, np.int64)]
+    while len(out) < count:
+        n = int(rng.integers(1, max_tiles + 1))
+        counts = rng.integers(0, 2 * max_atoms // max_tiles + 1, size=n)
+        counts[rng.random(n) < 0.25] = 0
+        if counts.sum() > max_atoms:
+            counts = counts * max_atoms // max(int(counts.sum()), 1)
+        off = np.zeros(n + 1, np.int64)
+        np.cumsum(counts, out=off[1:])
+        out.append(off)
+    return out
+
+
+def pack(arrays):
+    arrays = [np.asarray(a) for a in arrays]
+    idx = np.zeros(len(arrays) + 1, np.int64)
+    np.cumsum([a.size for a in arrays], out=idx[1:])
+    flat = np.concatenate([a.reshape(-1) for a in arrays]) if arrays else np.zeros(0)
+    return flat, idx
+
+
+def reference_assignment(ts, cfg):
+    """(lane_of_atom, tile_of_atom) exactly as the reference executors deliver atoms."""
+    n = ts.num_atoms
+    lane_of = np.full(n, -1, np.int64)
+    tile_of = np.full(n, -1, np.int64)
+    visits = np.zeros(n, np.int64)
+    if cfg.schedule is lw.ScheduleKind.MERGE_PATH:
+        def atom_fn(lane, tile, atom):
+            lane_of[atom], tile_of[atom] = lane, tile
+            visits[atom] += 1
+            return 0.0
+
+        lw.execute_merge_path(cfg, ts, atom_fn, lambda lane, tile, acc: None)
+    else:
+        def work_fn(lane, tile, atoms):
+            for a in atoms:
+                lane_of[a], tile_of[a] = lane, tile
+                visits[a] += 1
+
+        lw.execute_tile_major(cfg, ts, work_fn)
+    assert (visits == 1).all()
+    return lane_of, tile_of
+
+
+def make_schedules():
+    sets = tile_set_corpus(48, seed=1234)
+    lane_counts = [1, 2, 3, 5, 7, 13, 32, 64, 100]
+    search, parts, imbal, plans, tiles = [], [], [], [], []
+    assign_lane, assign_tile, assign_meta = [], [], []
+    gm_shapes = [(1, 1), (4, 4), (4, 7), (32, 32), (8, 3)]
+    for si, off in enumerate(sets):
+        ts = lw.TileSet(off)
+        total = ts.num_tiles + ts.num_atoms
+        search.append(np.array([lw.merge_path_search(d, ts) for d in range(total + 1)],
+                               np.int64).reshape(-1, 2))
+        for p in lane_counts:
+            parts.append(lw.merge_path_partition(ts, p))
+            for kind in lw.ScheduleKind:
+                shapes = gm_shapes if kind is lw.ScheduleKind.GROUP_MAPPED else [(32, 32)]
+                for gs, tpb in shapes:
+                    cfg = lw.ExecutorConfig(schedule=kind, lanes=p, group_size=gs,
+                                            tiles_per_block=tpb)
+                    imbal.append(lw.imbalance(ts, cfg).per_lane_atoms)
+                    if p in (1, 3, 7, 32) and si < 24:
+                        lo, to = reference_assignment(ts, cfg)
+                        assign_lane.append(lo)
+                        assign_tile.append(to)
+                        assign_meta.append([si, p, list(lw.ScheduleKind).index(kind), gs, tpb])
+        for tpb in (1, 3, 32):
+            nb = lw.schedules.num_blocks(ts, tpb)
+            for b in range(nb):
+                plan = lw.group_plan(ts, b, nb, tpb, block=b)
+                plans.append(plan.prefix)
+                tiles.append(np.array([lw.get_tile(plan, a) for a in range(plan.total_atoms)],
+                                      np.int64))
+    np.savez_compressed(
+        OUT / "schedules.npz",
+        sets=pack(sets)[0], sets_idx=pack(sets)[1], lane_counts=np.array(lane_counts),
+        search=pack(search)[0], search_idx=pack(search)[1],
+        parts=pack(parts)[0], parts_idx=pack(parts)[1],
+        imbal=pack(imbal)[0], imbal_idx=pack(imbal)[1],
+        gm_shapes=np.array(gm_shapes),
+        plans=pack(plans)[0], plans_idx=pack(plans)[1],
+        tiles=pack(tiles)[0], tiles_idx=pack(tiles)[1],
+        assign_lane=pack(assign_lane)[0], assign_tile=pack(assign_tile)[0],
+        assign_idx=pack(assign_lane)[1], assign_meta=np.array(assign_meta, np.int64),
+    )
+
+
+def make_spmv():
+    rng = np.random.default_rng(2024)
+    mats, xs, ys, meta = [], [], [], []
+    cfgs = []
+    for lanes in (9, 16, 64):
+        cfgs.append(("thread-mapped", lanes, 32, 32))
+        cfgs.append(("merge-path", lanes, 32, 32))
+        for gs in (4, 32, 256):
+            cfgs.append(("group-mapped", lanes, gs, gs))
+    for i in range(24):
+        rows = int(rng.integers(1, 120))
+        cols = int(rng.integers(1, 120))
+        nnz = int(rng.integers(0, min(rows * cols, 900) + 1))
+        m = lw.generate_random_csr(rows, cols, nnz, seed=int(rng.integers(1 << 30)))
+        integer = i % 2 == 0
+        if integer:
+            m.values = rng.integers(-4, 5, size=m.nnz).astype(np.float64)
+            x = rng.integers(-3, 4, size=cols).astype(np.float64)
+        else:
+            x = rng.random(cols)
+        for ci, (kind, lanes, gs, tpb) in enumerate(cfgs):
+            cfg = lw.ExecutorConfig(schedule=lw.ScheduleKind(kind), lanes=lanes, worker_threads=2,
+                                    group_size=gs, tiles_per_block=tpb)
+            ys.append(lw.spmv(m, x, cfg))
+            meta.append([i, ci, int(integer)])
+        mats.append(m)
+        xs.append(x)
+    np.savez_compressed(
+        OUT / "spmv.npz",
+        rows=np.array([m.rows for m in mats]), cols=np.array([m.cols for m in mats]),
+        off=pack([m.row_offsets for m in mats])[0], off_idx=pack([m.row_offsets for m in mats])[1],
+        col=pack([m.col_indices for m in mats])[0], col_idx=pack([m.col_indices for m in mats])[1],
+        val=pack([m.values for m in mats])[0],
+        x=pack(xs)[0], x_idx=pack(xs)[1],
+        y=pack(ys)[0], y_idx=pack(ys)[1], meta=np.array(meta),
+        cfg_kind=np.array([c[0] for c in cfgs]), cfg_lanes=np.array([c[1] for c in cfgs]),
+        cfg_gs=np.array([c[2] for c in cfgs]), cfg_tpb=np.array([c[3] for c in cfgs]),
+    )
+
+
+def make_generators():
+    out = {}
+    cases = [("random", (40, 30, 200, 1)), ("random", (300, 200, 5000, 7)),
+             ("random", (5000, 5000, 10000, 11)), ("random", (10, 10, 100, 3)),
+             ("power", (500, 8.0, 1.1, 3)), ("power", (2000, 16.0, 1.5, 4)),
+             ("power", (1000, 4.0, 3.0, 5))]
+    for k, (kind, args) in enumerate(cases):
+        m = lw.generate_random_csr(*args) if kind == "random" else lw.generate_power_law_csr(*args)
+        out[f"c{k}_kind"] = np.array(kind)
+        out[f"c{k}_args"] = np.array(args, dtype=np.float64)
+        out[f"c{k}_off"] = m.row_offsets
+        out[f"c{k}_col"] = m.col_indices
+        out[f"c{k}_val"] = m.values
+    out["count"] = np.array(len(cases))
+    np.savez_compressed(OUT / "generators.npz", **out)
+
+
+if __name__ == "__main__":
+    print("reference:", lw.__file__, "backend:", lw.backend_name())
+    make_schedules()
+    make_spmv()
+    make_generators()
+    for f in sorted(OUT.glob("*.npz")):
+        print(f.name, f.stat().st_size)

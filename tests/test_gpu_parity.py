@@ -1,0 +1,346 @@
+"""GPU parity suite: the sm_100a kernels (through the C ABI) against the reference.
+
+Every check compares the CUDA path with (a) golden vectors recorded from the
+reference itself (tests/golden) or (b) the C oracle on the same seeded inputs:
+  * schedule maps are bit-exact: merge-path partitions, group-plan prefixes,
+    per-lane atom counts (== executor.imbalance) and the (lane, tile) each atom
+    is processed by (== the reference executors), each atom exactly once;
+  * y is bit-exact on integer-valued data (fp32 and fp64, every schedule);
+  * otherwise |y - y_ref| <= rtol * sum_j |A_ij x_j| with rtol 1e-5 (fp32) and
+    1e-12 (fp64), the north star's tolerance (BASELINE.json).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import integer_csr, unpack
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2301_04792_b200 as lwb  # noqa: E402
+from paper_2301_04792_b200 import DeviceCsr, ExecutorConfig, ScheduleKind  # noqa: E402
+
+RTOL = {torch.float32: 1e-5, torch.float64: 1e-12}
+KINDS = {"thread-mapped": ScheduleKind.THREAD_MAPPED, "merge-path": ScheduleKind.MERGE_PATH,
+         "group-mapped": ScheduleKind.GROUP_MAPPED}
+
+
+def dev_csr(off, col, val, cols, dtype=torch.float64, offset_bits=32):
+    off = np.asarray(off, np.int64)
+    odt = torch.int32 if offset_bits == 32 else torch.int64
+    return DeviceCsr(len(off) - 1, int(cols),
+                     torch.as_tensor(off).to("cuda", odt),
+                     torch.as_tensor(np.asarray(col, np.int64)).to("cuda", torch.int32),
+                     torch.as_tensor(np.asarray(val, np.float64)).to("cuda", dtype))
+
+
+def run(m, x, kind, lanes=None, gs=32, tpb=None):
+    cfg = ExecutorConfig(schedule=KINDS[kind] if isinstance(kind, str) else kind, lanes=lanes,
+                         group_size=gs, tiles_per_block=tpb)
+    xt = torch.as_tensor(np.asarray(x, np.float64)).to("cuda", m.dtype)
+    return lwb.spmv(m, xt, cfg).double().cpu().numpy()
+
+
+def check_tol(y, off, col, val, x, dtype, y_ref=None):
+    if y_ref is None:
+        y_ref = oracle.spmv(off, col, val, x, "thread-mapped", lanes=1)
+    scale = oracle.abs_row_sums(off, col, val, x)
+    ok, worst = oracle.tolerance_ok(y, y_ref, scale, RTOL[dtype])
+    assert ok, f"tolerance exceeded: worst err/bound = {worst:.3g}"
+
+
+# ---- schedule maps (bit-exact) ----------------------------------------------------------
+
+@pytest.mark.parametrize("bits", [32, 64])
+def test_partition_matches_reference_golden(golden, bits):
+    g = golden["schedules"]
+    sets = golden.tile_sets()
+    lane_counts = list(g["lane_counts"])
+    k = 0
+    for off in sets:
+        odt = torch.int32 if bits == 32 else torch.int64
+        m = DeviceCsr(len(off) - 1, 1, torch.as_tensor(off).to("cuda", odt),
+                      torch.zeros(int(off[-1]), dtype=torch.int32, device="cuda"),
+                      torch.zeros(int(off[-1]), dtype=torch.float32, device="cuda"))
+        for p in lane_counts:
+            want = unpack(g["parts"], g["parts_idx"], k).reshape(-1, 2)
+            got = lwb.device_merge_path_partition(m, int(p)).cpu().numpy()
+            np.testing.assert_array_equal(got, want)
+            k += 1
+
+
+def test_partition_every_diagonal_matches_reference_search(golden):
+    """lanes = total makes every diagonal a split point: the full search table."""
+    g = golden["schedules"]
+    for s, off in enumerate(golden.tile_sets()):
+        want = unpack(g["search"], g["search_idx"], s).reshape(-1, 2)
+        total = len(off) - 1 + int(off[-1])
+        if total == 0:
+            continue
+        m = DeviceCsr(len(off) - 1, 1, torch.as_tensor(off).to("cuda", torch.int32),
+                      torch.zeros(int(off[-1]), dtype=torch.int32, device="cuda"),
+                      torch.zeros(int(off[-1]), dtype=torch.float32, device="cuda"))
+        got = lwb.device_merge_path_partition(m, total).cpu().numpy()
+        np.testing.assert_array_equal(got, want)
+
+
+def test_group_plan_prefix_matches_reference_golden(golden):
+    g = golden["schedules"]
+    k = 0
+    for off in golden.tile_sets():
+        ts = lwb.TileSet(off)
+        for tpb in (1, 3, 32):
+            nb = lwb.num_blocks(ts, tpb)
+            if nb == 0:
+                continue
+            got = lwb.device_group_plan_prefix(ts, tpb, device="cuda").cpu().numpy()
+            for b in range(nb):
+                want = unpack(g["plans"], g["plans_idx"], k)
+                np.testing.assert_array_equal(got[b, :len(want)], want)
+                assert (got[b, len(want):] == want[-1]).all()
+                k += 1
+
+
+def test_probe_assignment_matches_reference_executors(golden):
+    """Per-atom (lane, tile) and per-lane counts of the instrumented kernels equal
+    what the reference executors hand out (execute_tile_major/execute_merge_path)."""
+    g = golden["schedules"]
+    sets = golden.tile_sets()
+    kinds = list(ScheduleKind)[:3]
+    for k, (si, p, ki, gs, tpb) in enumerate(g["assign_meta"]):
+        off = sets[si]
+        nnz = int(off[-1])
+        if nnz == 0:
+            continue
+        m = DeviceCsr(len(off) - 1, 1, torch.as_tensor(off).to("cuda", torch.int32),
+                      torch.zeros(nnz, dtype=torch.int32, device="cuda"),
+                      torch.ones(nnz, dtype=torch.float64, device="cuda"))
+        cfg = ExecutorConfig(schedule=kinds[ki], lanes=int(p), group_size=int(gs),
+                             tiles_per_block=int(tpb))
+        x = torch.ones(1, dtype=torch.float64, device="cuda")
+        y, pr, lanes = lwb.spmv_probe(m, x, cfg)
+        np.testing.assert_array_equal(pr["atom_visits"], np.ones(nnz))
+        np.testing.assert_array_equal(pr["atom_lane"], unpack(g["assign_lane"], g["assign_idx"], k))
+        np.testing.assert_array_equal(pr["atom_tile"], unpack(g["assign_tile"], g["assign_idx"], k))
+        np.testing.assert_array_equal(y.cpu().numpy(), np.diff(off).astype(np.float64))
+        ref_counts = lwb.imbalance(lwb.TileSet(off), cfg).per_lane_atoms
+        np.testing.assert_array_equal(pr["lane_atoms"], ref_counts)
+
+
+@pytest.mark.parametrize("kind,gs", [("thread-mapped", 32), ("merge-path", 32),
+                                     ("group-mapped", 32), ("group-mapped", 256),
+                                     ("group-mapped", 128), ("group-mapped", 4)])
+def test_probe_auto_lanes_matches_oracle(kind, gs):
+    """At device-chosen lane counts (the production launch) the per-thread work
+    equals the oracle's assignment for that P, on a skewed power-law matrix."""
+    m = lwb.generate_power_law_csr(20000, 12.0, 1.2, seed=7)
+    dm = m.to_device("float32")
+    cfg = lwb.device_config(ExecutorConfig(schedule=KINDS[kind], group_size=gs), dm)
+    x = torch.ones(m.cols, dtype=torch.float32, device="cuda")
+    y, pr, lanes = lwb.spmv_probe(dm, x, cfg)
+    la, al, at = oracle.assignment(m.row_offsets, kind, lanes, gs, gs)
+    np.testing.assert_array_equal(pr["atom_visits"], np.ones(m.nnz))
+    np.testing.assert_array_equal(pr["lane_atoms"], la)
+    np.testing.assert_array_equal(pr["atom_lane"], al)
+    np.testing.assert_array_equal(pr["atom_tile"], at)
+
+
+# ---- y against the reference (golden) ------------------------------------------------------
+
+@pytest.mark.parametrize("bits", [32, 64])
+def test_spmv_fp64_matches_reference_golden(golden, bits):
+    g = golden["spmv"]
+    for (mi, ci, integer), yk in zip(g["meta"], range(len(g["meta"]))):
+        k, off, col, val, x, rows, cols = list(golden.spmv_cases())[mi]
+        want = unpack(g["y"], g["y_idx"], yk)
+        m = dev_csr(off, col, val, cols, torch.float64, bits)
+        kind = str(g["cfg_kind"][ci])
+        y = run(m, x, kind, int(g["cfg_lanes"][ci]), int(g["cfg_gs"][ci]), int(g["cfg_tpb"][ci]))
+        if integer:
+            np.testing.assert_array_equal(y, want)
+        else:
+            scale = oracle.abs_row_sums(off, col, val, x)
+            ok, worst = oracle.tolerance_ok(y, want, scale, 1e-12)
+            assert ok, (mi, kind, worst)
+
+
+# ---- integer data: bit-exact across schedules, lane counts and dtypes ---------------------
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_integer_bit_exact_all_schedules(dtype):
+    """Acceptance criterion 4 (reference tests/test_acceptance.py:136-166) on the GPU."""
+    rng = np.random.default_rng(88)
+    cfgs = [("thread-mapped", None, 32), ("merge-path", None, 32), ("group-mapped", None, 32),
+            ("group-mapped", None, 256), ("thread-mapped", 64, 32), ("merge-path", 64, 32),
+            ("group-mapped", 64, 4), ("group-mapped", 64, 32), ("group-mapped", 64, 256),
+            ("merge-path", 7, 32), ("group-mapped", None, 128), ("group-mapped", None, 64)]
+    for _ in range(40):
+        rows, cols = int(rng.integers(1, 513)), int(rng.integers(1, 513))
+        nnz = int(rng.integers(0, min(8192, rows * cols) + 1))
+        m = integer_csr(rng, rows, cols, nnz)
+        x = rng.integers(-3, 4, size=cols).astype(np.float64)
+        want = m.to_dense() @ x
+        dm = m.to_device(dtype)
+        for kind, lanes, gs in cfgs:
+            np.testing.assert_array_equal(run(dm, x, kind, lanes, gs, gs), want,
+                                          err_msg=f"{kind} lanes={lanes} gs={gs}")
+
+
+# ---- fp32 tolerance on the north-star inputs -----------------------------------------------
+
+@pytest.fixture(scope="module")
+def c1():
+    m = lwb.generate_random_csr(10_000, 10_000, 1_000_000, seed=1)
+    vals32 = m.values.astype(np.float32).astype(np.float64)
+    x = np.random.default_rng(42).random(m.cols).astype(np.float32).astype(np.float64)
+    return m, vals32, x
+
+
+@pytest.mark.parametrize("kind,gs", [("thread-mapped", 32), ("merge-path", 32),
+                                     ("group-mapped", 32), ("group-mapped", 256)])
+def test_c1_fp32_within_tolerance(c1, kind, gs):
+    m, vals32, x = c1
+    dm = m.to_device("float32")
+    y = run(dm, x, kind, None, gs, gs)
+    check_tol(y, m.row_offsets, m.col_indices, vals32, x, torch.float32)
+
+
+@pytest.mark.parametrize("skew", [3.0, 1.5, 1.1])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_power_law_sweep_within_tolerance(skew, dtype):
+    m = lwb.generate_power_law_csr(1 << 16, 16.0, skew, seed=4)
+    vals = m.values.astype(np.float32).astype(np.float64) if dtype == torch.float32 else m.values
+    x = np.random.default_rng(42).random(m.cols)
+    x = x.astype(np.float32).astype(np.float64) if dtype == torch.float32 else x
+    dm = m.to_device(dtype)
+    y_ref = oracle.spmv(m.row_offsets, m.col_indices, vals, x, "merge-path", threads=4)
+    for kind, gs in [("thread-mapped", 32), ("merge-path", 32), ("group-mapped", 32),
+                     ("group-mapped", 256)]:
+        check_tol(run(dm, x, kind, None, gs, gs), m.row_offsets, m.col_indices, vals, x, dtype,
+                  y_ref)
+
+
+def test_all_positive_long_rows_fp32():
+    """one fp32 accumulator fails 1e-5 at 7e5 positive terms;
+    fp64 accumulation keeps every schedule inside the bound."""
+    rows, per = 4, 700_000
+    off = np.arange(rows + 1, dtype=np.int64) * per
+    rng = np.random.default_rng(3)
+    col = np.tile(np.arange(per, dtype=np.int64), rows)
+    val = rng.random(rows * per).astype(np.float32).astype(np.float64)
+    x = rng.random(per).astype(np.float32).astype(np.float64)
+    m = dev_csr(off, col, val, per, torch.float32)
+    for kind in ("thread-mapped", "merge-path", "group-mapped"):
+        check_tol(run(m, x, kind), off, col, val, x, torch.float32)
+
+
+# ---- edge cases the reference tests -------------------------------------------------------
+
+@pytest.mark.parametrize("kind", ["thread-mapped", "merge-path", "group-mapped"])
+def test_edge_cases(kind):
+    cases = [
+        ([0, 0, 0, 0], [], [], 3),                 # all rows empty
+        ([0, 1], [0], [2.5], 1),                   # single atom
+        ([0, 2, 3], [0, 1, 1], [1.0, 2.0, 3.0], 2),  # reference 2x2 example -> [3, 3] with x=1
+        ([0, 0, 5, 5, 5], [0, 1, 2, 3, 4], [1.0] * 5, 5),
+    ]
+    for off, col, val, cols in cases:
+        m = dev_csr(off, col, val, cols, torch.float64)
+        x = np.ones(cols)
+        want = np.zeros(len(off) - 1)
+        for r in range(len(off) - 1):
+            want[r] = sum(val[a] * x[col[a]] for a in range(off[r], off[r + 1]))
+        for lanes in (None, 1, 2, 3, 100):
+            np.testing.assert_array_equal(run(m, x, kind, lanes), want)
+
+
+def test_dimension_mismatch_raises():
+    m = dev_csr([0, 1, 2], [0, 1], [1.0, 1.0], 2)
+    with pytest.raises(ValueError):
+        lwb.spmv(m, torch.ones(3, dtype=torch.float64, device="cuda"))
+    host = lwb.CsrMatrix(3, 3, np.arange(4), np.arange(3), np.ones(3))
+    with pytest.raises(ValueError):
+        lwb.spmv(host, np.ones(4))
+
+
+def test_host_operands_match_reference_api():
+    """spmv(CsrMatrix, ndarray) returns a float64 ndarray like the reference."""
+    m = lwb.CsrMatrix(2, 2, [0, 2, 3], [0, 1, 1], [1.0, 2.0, 3.0])
+    y = lwb.spmv(m, np.ones(2))
+    assert isinstance(y, np.ndarray) and y.dtype == np.float64
+    np.testing.assert_array_equal(y, [3.0, 3.0])
+    ident = lwb.CsrMatrix(6, 6, np.arange(7), np.arange(6), np.ones(6))
+    x = np.random.default_rng(0).random(6)
+    np.testing.assert_array_equal(lwb.spmv(ident, x), x)
+    for kind in ScheduleKind:
+        np.testing.assert_array_equal(lwb.spmv(ident, x, ExecutorConfig(schedule=kind, lanes=3)), x)
+
+
+@pytest.mark.parametrize("lanes", [None, 1, 3, 64, 1000])
+def test_one_giant_row_carries(lanes):
+    """One 3M-atom tile cut into many lanes/CTAs: ordered carry fix-up
+    (reference test_executor.py:145-155 at GPU scale)."""
+    n = 3_000_000
+    off = np.array([0, 5, n - 7, n - 7, n], np.int64)
+    col = np.concatenate([np.arange(5), np.arange(n - 12) % 1000, np.arange(7)])
+    rng = np.random.default_rng(1)
+    val = rng.integers(-3, 4, size=n).astype(np.float64)
+    x = rng.integers(-3, 4, size=1000).astype(np.float64)
+    m = dev_csr(off, col, val, 1000, torch.float64)
+    want = oracle.spmv(off, col, val, x, "thread-mapped", lanes=1)
+    np.testing.assert_array_equal(run(m, x, "merge-path", lanes), want)
+
+
+def test_merge_path_run_to_run_deterministic():
+    m = lwb.generate_power_law_csr(1 << 15, 32.0, 1.05, seed=9)
+    dm = m.to_device("float32")
+    x = torch.rand(m.cols, device="cuda")
+    cfg = ExecutorConfig(schedule=ScheduleKind.MERGE_PATH)
+    y0 = lwb.spmv(dm, x, cfg).clone()
+    for _ in range(5):
+        assert torch.equal(lwb.spmv(dm, x, cfg), y0)
+    for kind, gs in [(ScheduleKind.GROUP_MAPPED, 32), (ScheduleKind.GROUP_MAPPED, 256),
+                     (ScheduleKind.THREAD_MAPPED, 32)]:
+        c = ExecutorConfig(schedule=kind, group_size=gs)
+        a = lwb.spmv(dm, x, c).clone()
+        assert torch.equal(lwb.spmv(dm, x, c), a)
+
+
+# ---- generators ---------------------------------------------------------------------------
+
+def test_rmat_device_matches_c_oracle():
+    scale, ef, seed = 14, 16, 3
+    th = lwb.rmat_thresholds()
+    dm = lwb.generate_rmat_csr(scale, ef, seed, dtype="float64", chunk_edges=100_000)
+    off, col, val = oracle.rmat_csr(scale, ef, seed, th, threads=4)
+    np.testing.assert_array_equal(dm.row_offsets.cpu().numpy(), off)
+    np.testing.assert_array_equal(dm.col_indices.cpu().numpy(), col)
+    np.testing.assert_array_equal(dm.values.cpu().numpy(), val)
+
+
+def test_banded_device_matches_host():
+    host = lwb.generate_banded_csr(5000, 16, seed=2)
+    dm = lwb.generate_banded_device(5000, 16, seed=2, dtype="float64")
+    np.testing.assert_array_equal(dm.row_offsets.cpu().numpy(), host.row_offsets)
+    np.testing.assert_array_equal(dm.col_indices.cpu().numpy(), host.col_indices)
+    np.testing.assert_array_equal(dm.values.cpu().numpy(), host.values)
+
+
+# ---- full-size property: C3 at a bounded scale ----------------------------------------------
+
+@pytest.mark.parametrize("scale", [20])
+def test_rmat_work_oriented_matches_oracle(scale):
+    dm = lwb.generate_rmat_csr(scale, 16, seed=3, dtype="float32")
+    x = torch.rand(dm.cols, device="cuda")
+    y = lwb.spmv(dm, x, ExecutorConfig(schedule=ScheduleKind.WORK_ORIENTED)).double().cpu().numpy()
+    off = dm.row_offsets.cpu().numpy().astype(np.int64)
+    col = dm.col_indices.cpu().numpy().astype(np.int64)
+    val = dm.values.cpu().numpy().astype(np.float64)
+    xh = x.cpu().numpy().astype(np.float64)
+    y_ref = oracle.spmv(off, col, val, xh, "merge-path", threads=oracle.default_threads())
+    check_tol(y, off, col, val, xh, torch.float32, y_ref)
