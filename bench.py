@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--items", type=int, default=0,
+                    help="work_oriented items per lane (0 = library default)")
     return ap.parse_args()
 
 
@@ -68,61 +70,68 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + clock-event (throttle) reasons sampled through NVML every ~20 ms
+    while the timed region runs (the same counters nvidia-smi's
+    clocks.sm / clocks_event_reasons.* report)."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_s: float = 0.005):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.period = period_s
+        self.samples = []
+        self.reason_bits = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
         self._t = None
+        self.error = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._sample()
+            self._t = threading.Thread(target=self._loop, daemon=True)
             self._t.start()
-        except FileNotFoundError:
-            self.proc = None
+        except Exception as exc:  # pragma: no cover - depends on the box
+            self.error = repr(exc)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _sample(self):
+        nv = self._nv
+        self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+        self.reason_bits |= nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                self._sample()
+            except Exception as exc:  # pragma: no cover
+                self.error = repr(exc)
+                return
+            self._stop.wait(self.period)
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
+        self._stop.set()
+        if self._t is not None:
+            self._t.join(timeout=2)
             try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+                self._sample()
+            except Exception:
+                pass
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                mx.append(float(parts[2]))
-            except ValueError:
-                continue
-            for name, v in zip(names, parts[5:9]):
-                if v.lower() == "active":
-                    reasons.add(name)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0,
+                    "error": self.error}
+        reasons = sorted(k for k, bit in self.REASONS.items() if self.reason_bits & bit)
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples), "source": "nvml"}
 
 
 # ---------------------------------------------------------------------------------------
@@ -223,24 +232,29 @@ def our_arm(args):
     ws_bytes = lib.lw_spmv_workspace(_lib.LW_MERGE_PATH, A.rows, A.nnz, 0, Ac.dtype)
     ws = torch.empty(max(ws_bytes, 256), dtype=torch.uint8, device=dev)
     launches_per_step = 3 if sched is lwb.ScheduleKind.MERGE_PATH else 1
+    lanes = 0
+    if args.items and sched is lwb.ScheduleKind.MERGE_PATH:
+        lanes = -(-(A.rows + A.nnz) // args.items)
+        ws_bytes = lib.lw_spmv_workspace(_lib.LW_MERGE_PATH, A.rows, A.nnz, lanes, Ac.dtype)
+        ws = torch.empty(max(ws_bytes, 256), dtype=torch.uint8, device=dev)
 
     # one step, with the dominant kernel bracketed by events
     ev = []
 
     def step(record):
         if sched is lwb.ScheduleKind.MERGE_PATH:
-            _lib.check(lib.lw_spmv_work_oriented_phases(Ac, x.data_ptr(), y.data_ptr(), 0,
+            _lib.check(lib.lw_spmv_work_oriented_phases(Ac, x.data_ptr(), y.data_ptr(), lanes,
                                                         ws.data_ptr(), ws.numel(), 1, sp), "p1")
             if record:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-            _lib.check(lib.lw_spmv_work_oriented_phases(Ac, x.data_ptr(), y.data_ptr(), 0,
+            _lib.check(lib.lw_spmv_work_oriented_phases(Ac, x.data_ptr(), y.data_ptr(), lanes,
                                                         ws.data_ptr(), ws.numel(), 2, sp), "p2")
             if record:
                 e1 = torch.cuda.Event(enable_timing=True)
                 e1.record(stream)
                 ev.append((e0, e1))
-            _lib.check(lib.lw_spmv_work_oriented_phases(Ac, x.data_ptr(), y.data_ptr(), 0,
+            _lib.check(lib.lw_spmv_work_oriented_phases(Ac, x.data_ptr(), y.data_ptr(), lanes,
                                                         ws.data_ptr(), ws.numel(), 4, sp), "p3")
         else:
             if record:
@@ -297,7 +311,7 @@ def our_arm(args):
                    "l2": "inputs > L2 (2.2 GB matrix streamed per step); no flush"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
                      "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": None,
-                     "kernel": "k_wo_staged" if sched is lwb.ScheduleKind.MERGE_PATH else args.schedule,
+                     "kernel": "k_wo_chunk" if sched is lwb.ScheduleKind.MERGE_PATH else args.schedule,
                      "kernel_ms": round(kern_ms, 4), "alg_bytes": alg_bytes,
                      "peak_source": hbm_src, "frac_of_8TBps": round(achieved / 8000.0, 4)},
         "hbm_gbs_step": round(alg_bytes / (ms * 1e-3) / 1e9, 1),

@@ -8,6 +8,7 @@ the .so is missing or fails to load, every device entry point raises
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
@@ -113,7 +114,7 @@ def load(path: Path | str | None = None):
     with _lock:
         if _lib is not None:
             return _lib
-        p = Path(path) if path else LIB_PATH
+        p = Path(path) if path else Path(os.environ.get("LWB200_LIB", LIB_PATH))
         if not p.exists():
             _load_error = f"{p} not built (run __graft_entry__.build() or python -m paper_2301_04792_b200._build)"
             raise BackendUnavailable(_load_error)

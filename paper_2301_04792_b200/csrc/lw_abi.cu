@@ -191,6 +191,16 @@ int lw_spmv_host(int schedule, const lw_csr_t* H, const void* x_host, void* y_ho
     auto up = [](size_t b) { return (b + 255) / 256 * 256; };
     const size_t bytes = up(off_b) + up(col_b) + up(val_b) + up(x_b) + up(y_b) + up(ws_b);
     unsigned char* d = nullptr;
+    {
+        // keep freed staging memory mapped in the default pool between calls (the
+        // pool otherwise unmaps it at every synchronize and re-maps GBs next call)
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    }
     LW_TRY(cudaMallocAsync((void**)&d, bytes > 0 ? bytes : 256, s));
     unsigned char* p = d;
     void* d_off = p; p += up(off_b);

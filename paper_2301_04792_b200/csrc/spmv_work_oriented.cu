@@ -6,44 +6,65 @@
 // exactly merge_path_partition(ts, P). Ties consume the row boundary first, so an
 // empty row costs one item (schedules.py:81).
 //
-// Device mapping. A lane is one thread. Three kernels, all stream-ordered:
-//  1. k_merge_path_search: one binary search per CTA boundary (or per lane for
-//     the direct variant) over off[t]+t; the same search lw_merge_path_partition
-//     exports, bit-exact with schedules.merge_path_partition.
-//  2. k_wo_staged<IPT> (items <= IPT): a CTA of NT lanes owns NT*items
-//     consecutive diagonals. Its row ends and its contiguous atom range are staged
-//     through shared memory with coalesced loads (values*x[col] formed during the
-//     staging pass so all gathers of the CTA are in flight together); every thread
-//     then re-runs the merge-path search inside shared memory for its own diagonal
-//     and consumes its items sequentially. Rows completed inside a thread are
-//     assigned directly; the partial row a thread starts in is finished with a
-//     block-wide segmented scan of thread carries (deterministic order), and the
-//     CTA's trailing partial becomes one carry-out.
-//     k_wo_direct (items > IPT, i.e. caller-chosen small lane counts): each lane
-//     walks its slice straight from global memory, the reference loop verbatim
-//     in semantics (_fast.py:31-52), one carry per lane.
-//  3. k_carry_fixup: adds carry-outs to their rows in lane/CTA order — the
-//     device form of the serial fix-up kernels.py:90-91 / fixup_combine
+// Device mapping. A lane is one CTA (the merge path is "searched per CTA",
+// BASELINE.json north star); three stream-ordered kernels:
+//  1. k_merge_path_search: one binary search per chunk boundary over off[t]+t —
+//     the same search lw_merge_path_partition exports, bit-exact with
+//     schedules.merge_path_partition (with one chunk per lane the boundaries are
+//     exactly the partition at P lanes).
+//  2. k_wo_chunk: the even-share SpMV of each lane's slice, chunk by chunk
+//     (details above the kernel); the lane's trailing partial row becomes its
+//     carry-out (reference _fast.py:46-52).
+//  3. k_carry_fixup: adds carry-outs to their rows in lane order — the device
+//     form of the serial fix-up kernels.py:90-91 / fixup_combine
 //     (executor.py:212-221). Runs of carries into one row are summed in order,
 //     so results are run-to-run reproducible (no float atomics).
+#include <algorithm>
+#include <climits>
+#include <cstdlib>
+
 #include "lw_common.cuh"
 
 namespace lw {
 
-constexpr int WO_NT = 256;          // lanes per CTA
-constexpr int WO_IPT_AUTO = 8;      // items per lane when lanes are auto-sized
+// Chunk geometry shared by every dtype: a chunk is at most WO_S merge-path items
+// (rows + atoms) and its atoms sit in an 8-aligned window of WO_W atoms.
+constexpr int WO_W = 4096;
+constexpr int WO_S = WO_W - 16;
 constexpr unsigned WO_PHASE_PARTITION = 1, WO_PHASE_SPMV = 2, WO_PHASE_FIXUP = 4;
 
+// threads x atoms-per-thread covering the window: one 32-byte col_idx load and
+// one (fp32) or two (fp64) 32-byte value loads per thread. NT=512 x IPT=8 beat
+// 256x16, 256x8 (W=2048) and 512x16 (W=8192) on C3 (kernel log).
+template <class ValT>
+struct WoCfg;
+template <>
+struct WoCfg<float> {
+    static constexpr int NT = 512, IPT = 8;
+};
+template <>
+struct WoCfg<double> {
+    static constexpr int NT = 512, IPT = 8;
+};
+
 // ---- 1. partition ---------------------------------------------------------
+// Boundary b of lane l = b / J, chunk j = b % J sits on diagonal
+// min(l*items + min(j*S, items), total); with J = 1 this is exactly
+// schedules.merge_path_partition's min(k*items, total).
+__device__ __forceinline__ int64_t wo_bound_diag(int64_t b, int64_t J, int64_t items, int64_t S,
+                                                 int64_t total) {
+    const int64_t l = J == 1 ? b : b / J, j = b - l * J;
+    return min(l * items + min(j * S, items), total);
+}
+
 template <class OffT>
 __global__ void k_merge_path_search(const OffT* __restrict__ off, int64_t rows, int64_t nnz,
-                                    int64_t n_bounds, int64_t span,
+                                    int64_t n_bounds, int64_t J, int64_t items, int64_t S,
                                     int64_t* __restrict__ out_tile,
                                     int64_t* __restrict__ out_coords) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n_bounds) return;
-    const int64_t total = rows + nnz;
-    const int64_t d = min(k * span, total);
+    const int64_t d = wo_bound_diag(k, J, items, S, rows + nnz);
     int64_t lo = max((int64_t)0, d - nnz), hi = min(d, rows);
     // greatest t with off[t] <= d - t  (off[t]+t strictly increasing)
     while (lo < hi) {
@@ -58,160 +79,411 @@ __global__ void k_merge_path_search(const OffT* __restrict__ off, int64_t rows, 
     }
 }
 
-// ---- 2a. staged even-share SpMV ------------------------------------------------
+// ---- 2. chunked even-share SpMV -------------------------------------------------
+// One CTA per lane. A lane's slice of the merge path is cut into chunks of at
+// most WO_S items; chunk boundaries come from the partition kernel, so every
+// chunk's atoms [a0, a1) and completed rows [t0, t1) are known up front. Per
+// chunk:
+//   1. thread t owns the IPT consecutive atoms base + IPT*t ... of the 8-aligned
+//      window over [a0, a1) and fetches their col_idx / values with 32-byte
+//      vector loads (whole sectors, the warp reads contiguous bytes), issues its
+//      first row-end load, then all IPT gathers of x at once;
+//   2. the chunk's row ends are staged in shared memory and marked in a bit
+//      mask of segment heads;
+//   3. a block-wide segmented inclusive scan (thread-serial over IPT atoms,
+//      warp shuffles, then across warps) turns products into running row sums;
+//      each completed row reads its sum at its last atom and is written once
+//      (coalesced; empty rows get 0);
+//   4. the trailing partial row is carried to the lane's next chunk, and the
+//      lane's final partial becomes its carry-out.
+// The scan runs in the value precision: a chunk's partial sums pass through at
+// most IPT + 5 + NT/32 additions, far inside the 1e-5 (fp32) bound; partials
+// that cross chunks are carried in fp64.
+template <int NT>
 struct WoScan {
-    int key[WO_NT / kWarp];
-    double val[WO_NT / kWarp];
-    int pkey[WO_NT / kWarp];      // inclusive scan of warp aggregates
-    double pval[WO_NT / kWarp];
+    int has[NT / kWarp];
+    double val[NT / kWarp];
 };
 
-template <class OffT, class ValT, int IPT, bool PROBE>
-__global__ void __launch_bounds__(WO_NT)
-    k_wo_staged(Csr<OffT, ValT> A, const ValT* __restrict__ x, ValT* __restrict__ y,
-                int64_t lanes, int64_t items, const int64_t* __restrict__ cta_tile,
-                int64_t* __restrict__ carry_tile, double* __restrict__ carry_val,
-                Probe probe) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* s_prod = reinterpret_cast<double*>(smem_raw);                // [NT*IPT]
-    int32_t* s_end = reinterpret_cast<int32_t*>(s_prod + WO_NT * IPT);    // [NT*IPT]
-    __shared__ WoScan scan;
+template <class ValT>
+struct WoSmem {
+    static constexpr size_t end_off = 0;                                   // int32[WO_S]
+    static constexpr size_t seg_off = end_off + sizeof(int32_t) * WO_S;    // ValT[WO_W]
+    static constexpr size_t flag_off = seg_off + sizeof(ValT) * WO_W;      // uint32[W/32+2]
+    static constexpr size_t bytes = flag_off + sizeof(uint32_t) * (WO_W / 32 + 2);
+};
 
-    const int tid = threadIdx.x;
-    const int lane = tid & (kWarp - 1), warp = tid >> 5;
-    const int64_t c = blockIdx.x;
-    const int64_t total = A.rows + A.nnz;
-    const int64_t span = WO_NT * items;
-    const int64_t d0 = min(c * span, total), d1 = min((c + 1) * span, total);
-    const int64_t t0 = cta_tile[c], t1 = cta_tile[c + 1];
-    const int64_t a0 = d0 - t0, a1 = d1 - t1;
-    const int n_rows = (int)(t1 - t0), n_atoms = (int)(a1 - a0);
-
-    // stage row ends (relative to a0): s_end[i] = off[t0+1+i] - a0
-    for (int i = tid; i < n_rows; i += WO_NT) s_end[i] = (int32_t)(ld_off(A.off + t0 + 1 + i) - a0);
-
-    // stage products: coalesced streaming loads, then all gathers in flight
-    {
-        int32_t cidx[IPT];
-        ValT v[IPT];
+// 8 consecutive col_idx / values with 32-byte loads (sm_100 .v8.b32 / .v4.b64)
+__device__ __forceinline__ void ld8_col(const int32_t* p, int32_t* c) {
+    const uint64_t pol = policy_evict_first();
+    asm volatile(
+        "ld.global.nc.L1::no_allocate.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+        : "=r"(c[0]), "=r"(c[1]), "=r"(c[2]), "=r"(c[3]), "=r"(c[4]), "=r"(c[5]), "=r"(c[6]),
+          "=r"(c[7])
+        : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ void ld8_val(const float* p, float* v) {
+    const uint64_t pol = policy_evict_first();
+    uint32_t r[8];
+    asm volatile(
+        "ld.global.nc.L1::no_allocate.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7])
+        : "l"(p), "l"(pol));
 #pragma unroll
-        for (int k = 0; k < IPT; ++k) {
-            const int j = k * WO_NT + tid;
-            if (j < n_atoms) {
-                cidx[k] = ld_stream(A.col + a0 + j);
-                v[k] = ld_stream(A.val + a0 + j);
+    for (int k = 0; k < 8; ++k) v[k] = __uint_as_float(r[k]);
+}
+__device__ __forceinline__ void ld8_val(const double* p, double* v) {
+    const uint64_t pol = policy_evict_first();
+    unsigned long long r[8];
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.b64 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=l"(r[0]), "=l"(r[1]), "=l"(r[2]), "=l"(r[3]) : "l"(p), "l"(pol));
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.b64 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=l"(r[4]), "=l"(r[5]), "=l"(r[6]), "=l"(r[7]) : "l"(p + 4), "l"(pol));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __longlong_as_double((long long)r[k]);
+}
+
+template <class OffT, class ValT, bool PROBE, bool VEC>
+__global__ void __launch_bounds__(WoCfg<ValT>::NT)
+    k_wo_chunk(Csr<OffT, ValT> A, const ValT* __restrict__ x, ValT* __restrict__ y,
+               int64_t items, int64_t J, const int64_t* __restrict__ bound_tile,
+               int64_t* __restrict__ carry_tile, double* __restrict__ carry_val, Probe probe) {
+    constexpr int NT = WoCfg<ValT>::NT, IPT = WoCfg<ValT>::IPT;
+    constexpr int W = WO_W, S = WO_S;
+    static_assert(NT * IPT == W, "window must be NT*IPT atoms");
+    using SM = WoSmem<ValT>;
+    extern __shared__ __align__(16) unsigned char sm[];
+    int32_t* s_end = reinterpret_cast<int32_t*>(sm + SM::end_off);
+    ValT* s_seg = reinterpret_cast<ValT*>(sm + SM::seg_off);
+    uint32_t* s_flag = reinterpret_cast<uint32_t*>(sm + SM::flag_off);
+    __shared__ WoScan<NT> scan;
+
+    const int tid = threadIdx.x, lane = tid & (kWarp - 1), warp = tid >> 5;
+    const int64_t l = blockIdx.x;
+    const int64_t total = A.rows + A.nnz;
+    const int64_t lane_d0 = l * items;
+    int64_t run_row = -1;    // lane-level partial carried across chunks
+    double run_val = 0.0;
+    bool run_has = false;
+    int64_t lane_atoms = 0;
+
+    for (int64_t jc = 0; jc < J; ++jc) {
+        const int64_t d0 = min(lane_d0 + min(jc * S, items), total);
+        const int64_t d1 = min(lane_d0 + min((jc + 1) * S, items), total);
+        if (d0 >= d1) break;
+        const int64_t t0 = bound_tile[l * J + jc], t1 = bound_tile[l * J + jc + 1];
+        const int64_t a0 = d0 - t0;
+        const int n_rows = (int)(t1 - t0), n_atoms = (int)((d1 - t1) - a0);
+        const int64_t base = a0 & ~(int64_t)7;
+        const int w0 = (int)(a0 - base);     // window position of a0
+        const int w1 = w0 + n_atoms;         // one past the last atom
+        lane_atoms += n_atoms;
+
+        // zero the head mask (the previous chunk's readers finished at its last barrier)
+        if (tid <= W / 32 + 1) s_flag[tid] = 0u;
+
+        // 1. every global load of the chunk is issued before its first use
+        const int pos = IPT * tid;           // window position of my first atom
+        const int64_t g = base + pos;
+        ValT p[IPT];
+        const bool row0 = tid < n_rows;
+        int32_t e0 = 0;
+        {
+            int32_t c[IPT];
+            ValT v[IPT];
+#pragma unroll
+            for (int k = 0; k < IPT; ++k) { c[k] = 0; v[k] = (ValT)0; }
+            if (pos < w1) {
+                if (VEC && g + IPT <= A.nnz) {
+#pragma unroll
+                    for (int h = 0; h < IPT / 8; ++h) {
+                        ld8_col(A.col + g + 8 * h, c + 8 * h);
+                        ld8_val(A.val + g + 8 * h, v + 8 * h);
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < IPT; ++k)
+                        if (g + k < A.nnz) { c[k] = ld_stream(A.col + g + k); v[k] = ld_stream(A.val + g + k); }
+                }
+            }
+            if (row0) e0 = (int32_t)(ld_off(A.off + t0 + 1 + tid) - base);
+#pragma unroll
+            for (int k = 0; k < IPT; ++k) {
+                const bool in = pos + k >= w0 && pos + k < w1;
+                p[k] = in ? v[k] * ld_gather(x + c[k]) : (ValT)0;
             }
         }
-#pragma unroll
-        for (int k = 0; k < IPT; ++k) {
-            const int j = k * WO_NT + tid;
-            if (j < n_atoms) s_prod[j] = (double)v[k] * (double)ld_gather(x + cidx[k]);
+
+        // 2. row ends + segment-head bit mask
+        __syncthreads();
+        if (row0) {
+            s_end[tid] = e0;
+            if (e0 < W) atomicOr(&s_flag[e0 >> 5], 1u << (e0 & 31));
         }
-    }
-    __syncthreads();
-
-    // this lane's local coordinates: search inside shared memory
-    const int n_total = n_rows + n_atoms;
-    const int dl = (int)min((int64_t)tid * items, (int64_t)n_total);
-    const int dl_end = (int)min((int64_t)dl + items, (int64_t)n_total);
-    int lo = max(0, dl - n_atoms), hi = min(dl, n_rows);
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (s_end[mid - 1] <= dl - mid) lo = mid;
-        else hi = mid - 1;
-    }
-    int i = lo, j = dl - lo;
-    const int i_first = i, j_first = j;
-    const int64_t glane = c * WO_NT + tid;
-
-    double acc = 0.0, head = 0.0;
-    bool done_any = false;
-    for (int step = dl; step < dl_end; ++step) {
-        if (i < n_rows && s_end[i] <= j) {           // row boundary first on ties
-            if (!done_any) { head = acc; done_any = true; }
-            else y[t0 + i] = (ValT)acc;
-            acc = 0.0;
-            ++i;
-        } else {
-            acc += s_prod[j];
-            if (PROBE) probe_atom(probe, a0 + j, glane, t0 + i);
-            ++j;
+        for (int i = tid + NT; i < n_rows; i += NT) {   // chunks with more rows than threads
+            const int e = (int)(ld_off(A.off + t0 + 1 + i) - base);
+            s_end[i] = e;
+            if (e < W) atomicOr(&s_flag[e >> 5], 1u << (e & 31));
         }
-    }
-    if (PROBE && probe.lane_atoms && glane < lanes)
-        probe.lane_atoms[glane] = j - j_first;
+        __syncthreads();
 
-    // block-wide inclusive segmented scan of (tail row, tail partial)
-    int key = i;
-    double val = acc;
+        // 3. segmented scan: thread-serial, then warp shuffles, then across warps
+        uint32_t fl;
+        {
+            const uint64_t two = ((uint64_t)s_flag[(pos >> 5) + 1] << 32) | s_flag[pos >> 5];
+            fl = (uint32_t)(two >> (pos & 31)) & (uint32_t)((1ull << IPT) - 1ull);
+        }
+        bool has = fl != 0u;
+        ValT run = (ValT)0;
 #pragma unroll
-    for (int d = 1; d < kWarp; d <<= 1) {
-        const double ov = shfl_up(val, d);
-        const int ok = shfl_up(key, d);
-        if (lane >= d && ok == key) val += ov;
+        for (int k = 0; k < IPT; ++k) run = ((fl >> k) & 1u) ? p[k] : run + p[k];
+#pragma unroll
+        for (int d = 1; d < kWarp; d <<= 1) {
+            const ValT ov = shfl_up(run, d);
+            const int oh = shfl_up((int)has, d);
+            if (lane >= d) {
+                if (!has) run += ov;
+                has = has || oh;
+            }
+        }
+        if (lane == kWarp - 1) { scan.has[warp] = has; scan.val[warp] = (double)run; }
+        __syncthreads();
+        ValT wpre = (ValT)0;   // open segment entering my warp
+        {
+            bool h = false;
+            for (int w = warp - 1; w >= 0 && !h; --w) {
+                wpre += (ValT)scan.val[w];
+                h = scan.has[w];
+            }
+        }
+        ValT cin = shfl_up(run, 1);
+        const int hin = shfl_up((int)has, 1);
+        if (lane == 0) cin = wpre;
+        else if (!hin) cin += wpre;
+        {
+            ValT r = cin;
+#pragma unroll
+            for (int k = 0; k < IPT; ++k) {
+                r = ((fl >> k) & 1u) ? p[k] : r + p[k];
+                s_seg[pos + k] = r;
+            }
+        }
+        __syncthreads();
+
+        // 4. completed rows (coalesced), then the trailing partial
+        for (int i = tid; i < n_rows; i += NT) {
+            const int e = s_end[i];
+            const int st = i ? s_end[i - 1] : w0;
+            double v = e > st ? (double)s_seg[e - 1] : 0.0;
+            if (i == 0 && run_has && run_row == t0) v += run_val;
+            y[t0 + i] = (ValT)v;
+        }
+        if (PROBE) {
+            for (int w = tid; w < n_atoms; w += NT) {
+                const int wp = w0 + w;
+                int lo = 0, hi = n_rows;   // rows whose end <= wp come before the atom's row
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (s_end[mid] <= wp) lo = mid + 1;
+                    else hi = mid;
+                }
+                probe_atom(probe, a0 + w, l, t0 + lo);
+            }
+        }
+        {
+            const int st = n_rows ? s_end[n_rows - 1] : w0;
+            const bool tail = w1 > st;
+            const double tv = tail ? (double)s_seg[w1 - 1] : 0.0;
+            if (n_rows > 0) {
+                run_row = t1; run_val = tv; run_has = tail;
+            } else if (run_has && run_row == t1) {
+                run_val += tv;
+            } else {
+                run_row = t1; run_val = tv; run_has = tail;
+            }
+        }
+        __syncthreads();   // s_end / s_seg / s_flag are rewritten by the next chunk
     }
-    if (lane == kWarp - 1) { scan.key[warp] = key; scan.val[warp] = val; }
-    __syncthreads();
     if (tid == 0) {
-        int pk = scan.key[0];
-        double pv = scan.val[0];
-        scan.pkey[0] = pk; scan.pval[0] = pv;
-        for (int w = 1; w < WO_NT / kWarp; ++w) {
-            const int k2 = scan.key[w];
-            pv = (k2 == pk) ? pv + scan.val[w] : scan.val[w];
-            pk = k2;
-            scan.pkey[w] = pk; scan.pval[w] = pv;
-        }
-    }
-    __syncthreads();
-    if (warp > 0 && scan.pkey[warp - 1] == key) val += scan.pval[warp - 1];
-    // carry into this thread = inclusive value of the previous thread
-    double carry_in = shfl_up(val, 1);
-    if (lane == 0) carry_in = (warp > 0) ? scan.pval[warp - 1] : 0.0;
-    if (done_any) y[t0 + i_first] = (ValT)(head + carry_in);
-
-    if (tid == WO_NT - 1) {
-        // the CTA's trailing partial belongs to row t1 (if that row has atoms here)
-        const bool tail = (t1 < A.rows) && n_atoms > 0 &&
-                          (n_rows == 0 || s_end[n_rows - 1] < n_atoms);
-        carry_tile[c] = tail ? t1 : -1;
-        carry_val[c] = tail ? val : 0.0;
+        const bool live = run_has && run_row >= 0 && run_row < A.rows;
+        carry_tile[l] = live ? run_row : -1;
+        carry_val[l] = live ? run_val : 0.0;
+        if (PROBE && probe.lane_atoms) probe.lane_atoms[l] = lane_atoms;
     }
 }
 
-// ---- 2b. direct per-lane SpMV (large item counts) ------------------------------
-template <class OffT, class ValT, bool PROBE>
-__global__ void __launch_bounds__(256)
-    k_wo_direct(Csr<OffT, ValT> A, const ValT* __restrict__ x, ValT* __restrict__ y,
-                int64_t lanes, int64_t items, const int64_t* __restrict__ lane_tile,
-                int64_t* __restrict__ carry_tile, double* __restrict__ carry_val,
-                Probe probe) {
-    const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (l >= lanes) return;
+// ---- 2w. warp-autonomous chunk kernel ------------------------------------------------
+// One CTA per chunk (lane), one __syncthreads per chunk. The CTA streams the
+// chunk's atoms (32-byte loads), issues every gather, stages the chunk's row
+// ends in shared memory, and synchronises once. From there each warp works
+// alone on its WARP_ATOMS-atom slice of the window: it derives its segment-head
+// bits from the staged row ends, runs the segmented scan with shuffles, writes
+// the rows that end inside its slice, and emits a carry for the row its slice
+// ends in. Carries are indexed (chunk, warp), so they are ordered along the
+// merge path and k_carry_fixup adds them exactly like the lane carries of the
+// reference (kernels.py:90-91). The merge-path partition (the schedule) stays at
+// chunk granularity; the per-warp cut inside a chunk is a reduction detail.
+template <class OffT, class ValT, bool PROBE, bool VEC>
+__global__ void __launch_bounds__(WoCfg<ValT>::NT)
+    k_wo_warp(Csr<OffT, ValT> A, const ValT* __restrict__ x, ValT* __restrict__ y,
+              int64_t items, int64_t J, const int64_t* __restrict__ bound_tile,
+              int64_t* __restrict__ carry_tile, double* __restrict__ carry_val, Probe probe) {
+    constexpr int NT = WoCfg<ValT>::NT, IPT = WoCfg<ValT>::IPT;
+    constexpr int NW = NT / kWarp, W = WO_W, S = WO_S;
+    extern __shared__ __align__(16) unsigned char sm[];
+    int32_t* s_end = reinterpret_cast<int32_t*>(sm);                      // [S]
+    ValT* s_run = reinterpret_cast<ValT*>(sm + sizeof(int32_t) * S);      // [W] running sums
+
+    const int tid = threadIdx.x, lane = tid & (kWarp - 1), warp = tid >> 5;
+    const int64_t l = blockIdx.x;
     const int64_t total = A.rows + A.nnz;
-    int64_t t = lane_tile[l];
-    int64_t a = min(l * items, total) - t;
-    const int64_t t_end = lane_tile[l + 1];
-    const int64_t a_end = min((l + 1) * items, total) - t_end;
-    const int64_t a_begin = a;
-    double acc = 0.0;
-    for (; t < t_end; ++t) {
-        const int64_t re = ld_off(A.off + t + 1);
-        for (; a < re; ++a) {
-            acc = fma((double)__ldg(A.val + a), (double)ld_gather(x + __ldg(A.col + a)), acc);
-            if (PROBE) probe_atom(probe, a, l, t);
+    const int pos = IPT * tid;                 // window position of my first atom
+    const int wlo = IPT * kWarp * warp;        // my warp's slice [wlo, whi)
+    const int whi = wlo + IPT * kWarp;
+
+    for (int64_t jc = 0; jc < J; ++jc) {
+        const int64_t b = l * J + jc;
+        const int64_t d0 = min(l * items + min(jc * S, items), total);
+        const int64_t d1 = min(l * items + min((jc + 1) * S, items), total);
+        if (d0 >= d1) {
+            if (lane == 0) { carry_tile[b * NW + warp] = -1; carry_val[b * NW + warp] = 0.0; }
+            continue;
         }
-        y[t] = (ValT)acc;
-        acc = 0.0;
+        const int64_t t0 = bound_tile[b], t1 = bound_tile[b + 1];
+        const int64_t a0 = d0 - t0;
+        const int n_rows = (int)(t1 - t0), n_atoms = (int)((d1 - t1) - a0);
+        const int64_t base = a0 & ~(int64_t)7;
+        const int w0 = (int)(a0 - base), w1 = w0 + n_atoms;
+        if (PROBE && probe.lane_atoms && tid == 0) probe.lane_atoms[l] += n_atoms;
+
+        // ---- loads: atoms, gathers, row ends ----
+        const int64_t g = base + pos;
+        ValT p[IPT];
+        {
+            int32_t c[IPT];
+            ValT v[IPT];
+#pragma unroll
+            for (int k = 0; k < IPT; ++k) { c[k] = 0; v[k] = (ValT)0; }
+            if (pos < w1) {
+                if (VEC && g + IPT <= A.nnz) {
+#pragma unroll
+                    for (int h = 0; h < IPT / 8; ++h) {
+                        ld8_col(A.col + g + 8 * h, c + 8 * h);
+                        ld8_val(A.val + g + 8 * h, v + 8 * h);
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < IPT; ++k)
+                        if (g + k < A.nnz) { c[k] = ld_stream(A.col + g + k); v[k] = ld_stream(A.val + g + k); }
+                }
+            }
+            for (int i = tid; i < n_rows; i += NT)
+                s_end[i] = (int32_t)(ld_off(A.off + t0 + 1 + i) - base);
+#pragma unroll
+            for (int k = 0; k < IPT; ++k) {
+                const bool in = pos + k >= w0 && pos + k < w1;
+                p[k] = in ? v[k] * ld_gather(x + c[k]) : (ValT)0;
+            }
+        }
+        __syncthreads();   // row ends staged
+
+        // ---- my row ends: first row end >= pos (ends are nondecreasing) ----
+        int i_lo = 0;
+        {
+            int hi = n_rows;
+            while (i_lo < hi) {
+                const int mid = (i_lo + hi) >> 1;
+                if (s_end[mid] < pos) i_lo = mid + 1;
+                else hi = mid;
+            }
+        }
+        // head bits: a row end e in [pos, pos+IPT) starts a new segment at atom e
+        uint32_t fl = 0;
+        int i = i_lo;
+        for (; i < n_rows; ++i) {
+            const int e = s_end[i];
+            if (e >= pos + IPT) break;
+            fl |= 1u << (e - pos);
+        }
+        // ---- warp segmented scan (never crosses the warp's slice) ----
+        bool has = fl != 0u;
+        ValT run = (ValT)0;
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) run = ((fl >> k) & 1u) ? p[k] : run + p[k];
+#pragma unroll
+        for (int d = 1; d < kWarp; d <<= 1) {
+            const ValT ov = shfl_up(run, d);
+            const int oh = shfl_up((int)has, d);
+            if (lane >= d) {
+                if (!has) run += ov;
+                has = has || oh;
+            }
+        }
+        // carry into my atoms: the previous lane's inclusive running sum
+        ValT r = shfl_up(run, 1);
+        if (lane == 0) r = (ValT)0;
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) {
+            r = ((fl >> k) & 1u) ? p[k] : r + p[k];
+            s_run[pos + k] = r;
+        }
+        __syncwarp();
+
+        // ---- rows whose last atom lies in my IPT atoms (e in (pos, pos+IPT]) ----
+        {
+            int k = i_lo;
+            // rows ending exactly at pos belong to the previous thread, except
+            // the very first thread, which also owns rows ending at or before it
+            if (tid != 0)
+                while (k < n_rows && s_end[k] <= pos) ++k;
+            for (; k < n_rows; ++k) {
+                const int e = s_end[k];
+                if (e > pos + IPT) break;
+                const int st = k ? s_end[k - 1] : w0;
+                const ValT v = e > st ? s_run[e - 1] : (ValT)0;
+                y[t0 + k] = v;
+            }
+        }
+        if (PROBE) {
+#pragma unroll
+            for (int k = 0; k < IPT; ++k) {
+                const int wp = pos + k;
+                if (wp >= w0 && wp < w1) {
+                    int lo = 0, hi = n_rows;
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (s_end[mid] <= wp) lo = mid + 1;
+                        else hi = mid;
+                    }
+                    probe_atom(probe, base + wp, l, t0 + lo);
+                }
+            }
+        }
+        // ---- the warp's carry: the open segment at its last atom ----
+        if (lane == kWarp - 1) {
+            const int last = min(whi, w1) - 1;   // last atom position of the slice
+            int64_t ct = -1;
+            double cv = 0.0;
+            if (last >= max(wlo, w0)) {
+                // row of atom `last`: number of row ends <= last
+                int lo = 0, hi = n_rows;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (s_end[mid] <= last) lo = mid + 1;
+                    else hi = mid;
+                }
+                const bool open = lo == n_rows || s_end[lo] > last + 1;
+                if (open) {
+                    ct = t0 + lo;
+                    cv = (double)s_run[last];
+                }
+            }
+            carry_tile[b * NW + warp] = (ct >= 0 && ct < A.rows) ? ct : -1;
+            carry_val[b * NW + warp] = cv;
+        }
+        __syncthreads();   // s_end / s_run are rewritten by the next chunk
     }
-    const bool tail = a < a_end;
-    for (; a < a_end; ++a) {
-        acc = fma((double)__ldg(A.val + a), (double)ld_gather(x + __ldg(A.col + a)), acc);
-        if (PROBE) probe_atom(probe, a, l, t_end);
-    }
-    carry_tile[l] = tail ? t_end : -1;
-    carry_val[l] = acc;
-    if (PROBE && probe.lane_atoms) probe.lane_atoms[l] = a_end - a_begin;
 }
 
 // ---- 3. ordered carry fix-up -----------------------------------------------------
@@ -223,47 +495,60 @@ __global__ void k_carry_fixup(const int64_t* __restrict__ carry_tile,
     if (k >= n) return;
     const int64_t r = carry_tile[k];
     if (r < 0 || r >= rows) return;
-    if (k > 0 && carry_tile[k - 1] == r) return;   // not the head of its run
+    // Carry rows are nondecreasing along the path, with sentinels (-1) wherever
+    // a lane/warp ended on a row boundary; the head of a row's run is its first
+    // non-sentinel carry and it alone updates y[r] (no float atomics).
+    for (int64_t m = k - 1; m >= 0; --m) {
+        const int64_t t = carry_tile[m];
+        if (t == r) return;   // not the head of its run
+        if (t >= 0) break;
+    }
     double s = 0.0;
-    for (int64_t m = k; m < n && carry_tile[m] == r; ++m) s += carry_val[m];
+    for (int64_t m = k; m < n; ++m) {
+        const int64_t t = carry_tile[m];
+        if (t < 0) continue;
+        if (t != r) break;
+        s += carry_val[m];
+    }
     y[r] = (ValT)((double)y[r] + s);
 }
 
 // ---- host side -------------------------------------------------------------------
 struct WoPlan {
-    int64_t total, lanes, items;
-    int ipt;          // 8, 16 = staged variant; 0 = direct
-    int64_t n_units;  // CTAs (staged) or lanes (direct): carry slots
+    int64_t total, lanes, items, J;
 };
 
 static WoPlan wo_plan(int64_t rows, int64_t nnz, int64_t lanes) {
     WoPlan p{};
     p.total = rows + nnz;
-    if (lanes <= 0) lanes = p.total > 0 ? ceil_div(p.total, WO_IPT_AUTO) : 1;
+    if (lanes <= 0) lanes = p.total > 0 ? ceil_div(p.total, WO_S) : 1;
     p.lanes = lanes;
     p.items = p.total > 0 ? ceil_div(p.total, lanes) : 0;
-    if (p.items <= 8) p.ipt = 8;
-    else if (p.items <= 16) p.ipt = 16;
-    else p.ipt = 0;
-    p.n_units = p.ipt ? ceil_div(lanes, WO_NT) : lanes;
+    p.J = p.items > 0 ? ceil_div(p.items, WO_S) : 1;
     return p;
 }
 
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// carry slots: one per (chunk, warp) for the warp kernel (the largest layout)
+constexpr int WO_MAX_NW = 16;
+static size_t wo_carries(const WoPlan& p) { return (size_t)(p.lanes * p.J) * WO_MAX_NW; }
+
 size_t wo_workspace(int64_t rows, int64_t nnz, int64_t lanes) {
     const WoPlan p = wo_plan(rows, nnz, lanes);
-    const size_t n = (size_t)p.n_units;
-    return align_up((n + 1) * 8, 256) + align_up(n * 8, 256) + align_up(n * 8, 256);
+    const size_t nb = (size_t)(p.lanes * p.J + 1), nc = wo_carries(p);
+    return align_up(nb * 8, 256) + align_up(nc * 8, 256) + align_up(nc * 8, 256);
 }
 
+int64_t wo_lanes(int64_t rows, int64_t nnz, int64_t lanes) { return wo_plan(rows, nnz, lanes).lanes; }
+
 template <class OffT>
-static int launch_search(const OffT* off, int64_t rows, int64_t nnz, int64_t n_bounds,
-                         int64_t span, int64_t* out_tile, int64_t* out_coords,
+static int launch_search(const OffT* off, int64_t rows, int64_t nnz, int64_t n_bounds, int64_t J,
+                         int64_t items, int64_t S, int64_t* out_tile, int64_t* out_coords,
                          cudaStream_t s) {
     const int NT = 256;
-    k_merge_path_search<OffT><<<ceil_div(n_bounds, NT), NT, 0, s>>>(off, rows, nnz, n_bounds, span,
-                                                                 out_tile, out_coords);
+    k_merge_path_search<OffT><<<ceil_div(n_bounds, NT), NT, 0, s>>>(off, rows, nnz, n_bounds, J, items,
+                                                                 S, out_tile, out_coords);
     LW_LAUNCH_CHECK();
     return LW_OK;
 }
@@ -274,60 +559,103 @@ int merge_path_partition(int64_t rows, int64_t nnz, const void* off, int bits, i
     const int64_t total = rows + nnz;
     const int64_t items = total > 0 ? ceil_div(total, lanes) : 0;
     if (bits == 32)
-        return launch_search<int32_t>((const int32_t*)off, rows, nnz, lanes + 1, items, nullptr, coords, s);
-    return launch_search<int64_t>((const int64_t*)off, rows, nnz, lanes + 1, items, nullptr, coords, s);
+        return launch_search<int32_t>((const int32_t*)off, rows, nnz, lanes + 1, 1, items, items,
+                                      nullptr, coords, s);
+    return launch_search<int64_t>((const int64_t*)off, rows, nnz, lanes + 1, 1, items, items, nullptr,
+                                  coords, s);
+}
+
+template <class OffT, class ValT, bool PR, bool VEC>
+static int launch_chunk(const Csr<OffT, ValT>& a, const ValT* x, ValT* y, const WoPlan& p,
+                        const int64_t* tiles, int64_t* c_tile, double* c_val, const Probe& pr,
+                        cudaStream_t s) {
+    auto kern = k_wo_chunk<OffT, ValT, PR, VEC>;
+    constexpr size_t smem = WoSmem<ValT>::bytes;
+    static bool attr = false;   // one-time opt-in above the 48 KB default
+    if (!attr) {
+        LW_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    kern<<<(unsigned)p.lanes, WoCfg<ValT>::NT, smem, s>>>(a, x, y, p.items, p.J, tiles, c_tile,
+                                                         c_val, pr);
+    LW_LAUNCH_CHECK();
+    return LW_OK;
+}
+
+template <class Kern>
+static int set_smem(Kern kern, size_t smem, bool& done) {
+    if (!done) {   // one-time opt-in above the 48 KB default
+        LW_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        done = true;
+    }
+    return LW_OK;
+}
+
+// Kernel variant for the SpMV phase: 'c' (default) k_wo_chunk, 'v' k_wo_warp.
+// LW_WO_KERNEL overrides it for A/B runs (DESIGN.md records the measurements).
+static char wo_kind() {
+    static const char* e = getenv("LW_WO_KERNEL");
+    return (e && e[0] == 'v') ? 'v' : 'c';
 }
 
 template <class OffT, class ValT>
 static int launch_wo(const lw_csr_t* A, const void* x, void* y, const WoPlan& p, void* ws,
                      const lw_probe_t* probe, unsigned phases, cudaStream_t s) {
+    constexpr int NT = WoCfg<ValT>::NT, NW = NT / kWarp;
     Csr<OffT, ValT> a{A->rows, A->cols, A->nnz, (const OffT*)A->row_offsets,
                       A->col_indices, (const ValT*)A->values};
-    const size_t n = (size_t)p.n_units;
+    const size_t nb = (size_t)(p.lanes * p.J + 1), nc = wo_carries(p);
     unsigned char* w = (unsigned char*)ws;
     int64_t* tiles = (int64_t*)w;
-    int64_t* c_tile = (int64_t*)(w + align_up((n + 1) * 8, 256));
-    double* c_val = (double*)(w + align_up((n + 1) * 8, 256) + align_up(n * 8, 256));
+    int64_t* c_tile = (int64_t*)(w + align_up(nb * 8, 256));
+    double* c_val = (double*)(w + align_up(nb * 8, 256) + align_up(nc * 8, 256));
     Probe pr{};
     if (probe) pr = Probe{probe->lane_atoms, probe->atom_lane, probe->atom_tile, probe->atom_visits};
-    if (n > 0x7fffffff) return LW_E_UNSUPPORTED;
+    if (p.lanes > 0x7fffffff) return LW_E_UNSUPPORTED;
+    // 32-byte vector loads need 32-byte aligned col_idx / values
+    const bool vec = ((uintptr_t)A->col_indices % 32 == 0) && ((uintptr_t)A->values % 32 == 0);
+    const char kind = wo_kind();
+    // carries the fix-up walks: (chunk, warp) for 'v', lanes otherwise
+    const int64_t n_carry = kind == 'v' ? (int64_t)(nb - 1) * NW : p.lanes;
 
     if (phases & WO_PHASE_PARTITION) {
-        // CTA boundaries (staged) or lane boundaries (direct)
-        const int64_t span = p.ipt ? (int64_t)WO_NT * p.items : p.items;
-        int rc = launch_search<OffT>(a.off, a.rows, a.nnz, n + 1, span, tiles, nullptr, s);
+        int rc = launch_search<OffT>(a.off, a.rows, a.nnz, (int64_t)nb, p.J, p.items, WO_S, tiles,
+                                     nullptr, s);
         if (rc) return rc;
     }
     if (phases & WO_PHASE_SPMV) {
         if (probe && pr.lane_atoms) LW_TRY(cudaMemsetAsync(pr.lane_atoms, 0, p.lanes * 8, s));
-        if (p.ipt) {
-            const size_t smem = (size_t)WO_NT * p.ipt * (sizeof(double) + sizeof(int32_t));
-#define LW_WO_LAUNCH(IPT, PR)                                                                  \
-    do {                                                                                       \
-        auto kern = k_wo_staged<OffT, ValT, IPT, PR>;                                          \
-        static bool attr_set = false;                                                          \
-        if (!attr_set && smem > 48 * 1024) {                                                   \
-            LW_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                                        (int)(WO_NT * IPT * 12)));                            \
-            attr_set = true;                                                                   \
-        }                                                                                      \
-        kern<<<(unsigned)n, WO_NT, smem, s>>>(a, (const ValT*)x, (ValT*)y, p.lanes, p.items, tiles, \
-                                            c_tile, c_val, pr);                                \
-    } while (0)
-            if (p.ipt == 8) { if (probe) LW_WO_LAUNCH(8, true); else LW_WO_LAUNCH(8, false); }
-            else            { if (probe) LW_WO_LAUNCH(16, true); else LW_WO_LAUNCH(16, false); }
-#undef LW_WO_LAUNCH
-        } else {
-            const int NT = 256;
-            if (probe)
-                k_wo_direct<OffT, ValT, true><<<ceil_div(n, NT), NT, 0, s>>>(a, (const ValT*)x, (ValT*)y, p.lanes, p.items, tiles, c_tile, c_val, pr);
-            else
-                k_wo_direct<OffT, ValT, false><<<ceil_div(n, NT), NT, 0, s>>>(a, (const ValT*)x, (ValT*)y, p.lanes, p.items, tiles, c_tile, c_val, pr);
+        const ValT* xv = (const ValT*)x;
+        ValT* yv = (ValT*)y;
+        const bool P = probe != nullptr;
+        int rc = LW_OK;
+        switch (kind) {
+            case 'c':
+                if (P) rc = vec ? launch_chunk<OffT, ValT, true, true>(a, xv, yv, p, tiles, c_tile, c_val, pr, s)
+                                : launch_chunk<OffT, ValT, true, false>(a, xv, yv, p, tiles, c_tile, c_val, pr, s);
+                else   rc = vec ? launch_chunk<OffT, ValT, false, true>(a, xv, yv, p, tiles, c_tile, c_val, pr, s)
+                                : launch_chunk<OffT, ValT, false, false>(a, xv, yv, p, tiles, c_tile, c_val, pr, s);
+                break;
+            default: {
+                constexpr size_t smem = sizeof(int32_t) * WO_S + sizeof(ValT) * WO_W;
+                static bool done[4];
+                const int idx = (P ? 2 : 0) + (vec ? 1 : 0);
+#define LW_WOV(PR, VEC)                                                                              \
+    {                                                                                                \
+        auto kern = k_wo_warp<OffT, ValT, PR, VEC>;                                                  \
+        if ((rc = set_smem(kern, smem, done[idx]))) return rc;                                       \
+        kern<<<(unsigned)p.lanes, NT, smem, s>>>(a, xv, yv, p.items, p.J, tiles, c_tile, c_val, pr); \
+    }
+                if (P) { if (vec) LW_WOV(true, true) else LW_WOV(true, false) }
+                else   { if (vec) LW_WOV(false, true) else LW_WOV(false, false) }
+#undef LW_WOV
+            }
         }
+        if (rc) return rc;
         LW_LAUNCH_CHECK();
     }
     if (phases & WO_PHASE_FIXUP) {
-        k_carry_fixup<ValT><<<ceil_div(n, 256), 256, 0, s>>>(c_tile, c_val, (int64_t)n, (ValT*)y, a.rows);
+        k_carry_fixup<ValT><<<ceil_div(n_carry, 256), 256, 0, s>>>(c_tile, c_val, n_carry, (ValT*)y, a.rows);
         LW_LAUNCH_CHECK();
     }
     return LW_OK;
@@ -346,7 +674,5 @@ int spmv_work_oriented(const lw_csr_t* A, const void* x, void* y, int64_t lanes,
     return o32 ? launch_wo<int32_t, double>(A, x, y, p, ws, probe, phases, s)
                : launch_wo<int64_t, double>(A, x, y, p, ws, probe, phases, s);
 }
-
-int64_t wo_lanes(int64_t rows, int64_t nnz, int64_t lanes) { return wo_plan(rows, nnz, lanes).lanes; }
 
 }  // namespace lw

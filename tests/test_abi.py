@@ -57,7 +57,7 @@ def test_invalid_arguments_are_rejected_without_a_device(lib):
     assert lib.lw_auto_lanes(2, 10, 10, 0, 32, ctypes.byref(out)) == _lib.LW_E_INVALID_ARG
     assert lib.lw_auto_lanes(1, -1, 10, 32, 32, ctypes.byref(out)) == _lib.LW_E_INVALID_ARG
     assert lib.lw_auto_lanes(1, 10, 0, 32, 32, ctypes.byref(out)) == 0
-    assert out.value == 2  # ceil((10 + 0) / 8) lanes of the staged merge-path kernel
+    assert out.value == 1  # one 2040-item chunk (CTA) covers 10 rows
     a = _lib.LwCsr()
     a.rows, a.cols, a.nnz, a.offset_bits, a.dtype = 2, 2, 2, 16, 0
     assert lib.lw_spmv_thread_mapped(ctypes.byref(a), None, None, 0, None, 0) == _lib.LW_E_INVALID_ARG
