@@ -61,6 +61,20 @@ def parse():
     return ap.parse_args()
 
 
+def ncu_traffic(workload: str, dtype: str, schedule: str):
+    """DRAM bytes per launch of the dominant kernel from the newest committed
+    ncu --set full capture (profiles/*/ncu_traffic.json) for this workload."""
+    best = None
+    for f in sorted((ROOT / "profiles").glob("*/ncu_traffic.json")):
+        try:
+            d = json.loads(f.read_text())
+        except Exception:
+            continue
+        if d.get("workload") == workload and d.get("dtype") == dtype and d.get("schedule") == schedule:
+            best = (int(d["traffic_bytes_per_launch"]), str(f.relative_to(ROOT)))
+    return best
+
+
 def peaks():
     try:
         d = json.loads(PEAKS_FILE.read_text())
@@ -300,6 +314,9 @@ def our_arm(args):
     alg_bytes = A.algorithmic_bytes()
     hbm, hbm_src = peaks()
     achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
+    workload = f"rmat{args.scale}-ef{args.edge_factor}-seed{args.seed}"
+    tr = ncu_traffic(workload, "f32" if args.dtype == "fp32" else "f64", args.schedule) if world == 1 else None
+    traffic = tr[0] if tr else None
     line = {
         "metric": METRIC, "value": round(gflops, 3), "unit": "GFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4),
@@ -310,10 +327,11 @@ def our_arm(args):
                    "parallelism": f"rows{world}" if world > 1 else "single",
                    "l2": "inputs > L2 (2.2 GB matrix streamed per step); no flush"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
-                     "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": None,
+                     "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
                      "kernel": "k_wo_chunk" if sched is lwb.ScheduleKind.MERGE_PATH else args.schedule,
                      "kernel_ms": round(kern_ms, 4), "alg_bytes": alg_bytes,
-                     "peak_source": hbm_src, "frac_of_8TBps": round(achieved / 8000.0, 4)},
+                     "peak_source": hbm_src, "frac_of_8TBps": round(achieved / 8000.0, 4),
+                     "traffic_source": tr[1] if tr else None},
         "hbm_gbs_step": round(alg_bytes / (ms * 1e-3) / 1e9, 1),
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks.summary(),

@@ -144,6 +144,18 @@ __device__ __forceinline__ void ld8_val(const double* p, double* v) {
     for (int k = 0; k < 8; ++k) v[k] = __longlong_as_double((long long)r[k]);
 }
 
+// IPT (= 8) consecutive values into shared memory with 16-byte stores
+__device__ __forceinline__ void store_vec16(float* dst, const float* v) {
+    float4* d = reinterpret_cast<float4*>(dst);
+    d[0] = make_float4(v[0], v[1], v[2], v[3]);
+    d[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+__device__ __forceinline__ void store_vec16(double* dst, const double* v) {
+    double2* d = reinterpret_cast<double2*>(dst);
+#pragma unroll
+    for (int h = 0; h < 4; ++h) d[h] = make_double2(v[2 * h], v[2 * h + 1]);
+}
+
 template <class OffT, class ValT, bool PROBE, bool VEC>
 __global__ void __launch_bounds__(WoCfg<ValT>::NT)
     k_wo_chunk(Csr<OffT, ValT> A, const ValT* __restrict__ x, ValT* __restrict__ y,
@@ -152,6 +164,7 @@ __global__ void __launch_bounds__(WoCfg<ValT>::NT)
     constexpr int NT = WoCfg<ValT>::NT, IPT = WoCfg<ValT>::IPT;
     constexpr int W = WO_W, S = WO_S;
     static_assert(NT * IPT == W, "window must be NT*IPT atoms");
+    static_assert(IPT == 8, "store_vec16 writes 8 values");
     using SM = WoSmem<ValT>;
     extern __shared__ __align__(16) unsigned char sm[];
     int32_t* s_end = reinterpret_cast<int32_t*>(sm + SM::end_off);
@@ -262,12 +275,15 @@ __global__ void __launch_bounds__(WoCfg<ValT>::NT)
         if (lane == 0) cin = wpre;
         else if (!hin) cin += wpre;
         {
+            // running sums, stored with 16-byte vector stores (a thread's IPT
+            // consecutive slots; scalar stores would be an 8-way bank conflict)
             ValT r = cin;
 #pragma unroll
             for (int k = 0; k < IPT; ++k) {
                 r = ((fl >> k) & 1u) ? p[k] : r + p[k];
-                s_seg[pos + k] = r;
+                p[k] = r;
             }
+            store_vec16(s_seg + pos, p);
         }
         __syncthreads();
 
