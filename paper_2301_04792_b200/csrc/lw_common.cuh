@@ -42,6 +42,13 @@ __device__ __forceinline__ void probe_atom(const Probe& p, int64_t atom, int64_t
 }
 
 // ---- cache-policy loads --------------------------------------------------
+// Loads of read-only operands; LW_VOLATILE_LOADS pins their program order
+// (A/B switch: non-volatile lets ptxas hoist/batch them).
+#ifdef LW_VOLATILE_LOADS
+#define LW_LDASM asm volatile
+#else
+#define LW_LDASM asm
+#endif
 // Streaming operands (col_idx, values) are touched once per SpMV: keep them out
 // of L1 and mark them evict-first in L2 so the gathered x (reused across rows)
 // stays resident in the 126 MB L2 (policy via createpolicy + .L2::cache_hint).
@@ -57,32 +64,32 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 }
 __device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
     int32_t v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
+    LW_LDASM("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
                  : "=r"(v) : "l"(p), "l"(policy_evict_first()));
     return v;
 }
 __device__ __forceinline__ float ld_stream(const float* p) {
     float v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;"
+    LW_LDASM("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;"
                  : "=f"(v) : "l"(p), "l"(policy_evict_first()));
     return v;
 }
 __device__ __forceinline__ double ld_stream(const double* p) {
     double v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+    LW_LDASM("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
                  : "=d"(v) : "l"(p), "l"(policy_evict_first()));
     return v;
 }
 // Gathered x: read-only path, L1-allocating, evict-last in L2.
 __device__ __forceinline__ float ld_gather(const float* p) {
     float v;
-    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;"
+    LW_LDASM("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;"
                  : "=f"(v) : "l"(p), "l"(policy_evict_last()));
     return v;
 }
 __device__ __forceinline__ double ld_gather(const double* p) {
     double v;
-    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;"
+    LW_LDASM("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;"
                  : "=d"(v) : "l"(p), "l"(policy_evict_last()));
     return v;
 }

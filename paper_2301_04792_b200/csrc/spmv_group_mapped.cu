@@ -25,10 +25,39 @@
 //    monotone tile advance (_fast.py:75-76) and atomic adds into a zeroed y (the
 //    reference's pre-zeroed y += v*x, kernels.py:63 / _fast.py:77).
 #include <climits>
+#include <type_traits>
 
 #include "lw_common.cuh"
 
 namespace lw {
+
+#ifndef LW_GU
+#define LW_GU 4
+#endif
+constexpr int GU = LW_GU;     // member-stride steps whose loads are in flight together
+constexpr int GU_LONG = 64;  // blocks with >= GU_LONG*group atoms use the GU-step loop
+
+// Products of the atoms a member takes in GU consecutive member-stride steps
+// (local atoms k0 + u*STRIDE + m): every col/val load first, then every gather.
+template <class ValT, int U, int STRIDE, class OffT>
+__device__ __forceinline__ void gather_steps(const Csr<OffT, ValT>& A, const ValT* __restrict__ x,
+                                             int64_t base, OffT k0, int m, OffT total,
+                                             double (&p)[U]) {
+    int32_t c[U];
+    ValT v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const OffT k = k0 + u * STRIDE + m;
+        const bool valid = k < total;
+        c[u] = valid ? ld_stream(A.col + base + k) : 0;
+        v[u] = valid ? ld_stream(A.val + base + k) : (ValT)0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const bool valid = k0 + u * STRIDE + m < total;
+        p[u] = valid ? (double)v[u] * (double)ld_gather(x + c[u]) : 0.0;
+    }
+}
 
 // ---- warp tiles -------------------------------------------------------------------
 template <class OffT, class ValT, bool PROBE>
@@ -60,28 +89,36 @@ __global__ void __launch_bounds__(256)
         const int64_t base = (int64_t)shfl(lo_off, 0);
         s_acc[warp][lane] = 0.0;
         __syncwarp();
-        for (OffT k0 = 0; k0 < total; k0 += kWarp) {
-            const OffT k = k0 + lane;
-            const bool valid = k < total;
-            // get_tile: largest t < tc with excl[t] <= k (empty tiles never win)
-            int t = 0;
+        // U member-stride steps per iteration (lane takes local atoms k0+u*32+lane),
+        // all their loads and gathers in flight before the first reduction; U = GU
+        // only for long blocks (short ones would waste the padded steps)
+        auto steps = [&](auto uc) {
+          constexpr int U = decltype(uc)::value;
+          for (OffT k0 = 0; k0 < total; k0 += U * kWarp) {
+            double p[U];
+            gather_steps<ValT, U, kWarp>(A, x, base, k0, lane, total, p);
 #pragma unroll
-            for (int s = kWarp / 2; s >= 1; s >>= 1) {
-                const OffT e = shfl(excl, t + s);
-                if (t + s < tc && e <= k) t += s;
+            for (int u = 0; u < U; ++u) {
+                const OffT k = k0 + u * kWarp + lane;
+                const bool valid = k < total;
+                // get_tile: largest t < tc with excl[t] <= k (empty tiles never win)
+                int t = 0;
+#pragma unroll
+                for (int s = kWarp / 2; s >= 1; s >>= 1) {
+                    const OffT e = shfl(excl, t + s);
+                    if (t + s < tc && e <= k) t += s;
+                }
+                if (PROBE && valid) { probe_atom(probe, base + k, glane, tb + t); ++mine; }
+                const int key = valid ? t : INT_MAX;
+                const double sum = warp_segsum_to_head(p[u], key, lane);
+                const int prev = shfl_up(key, 1);
+                if (valid && (lane == 0 || prev != key)) s_acc[warp][t] += sum;
+                __syncwarp();
             }
-            double p = 0.0;
-            if (valid) {
-                const int64_t a = base + k;
-                p = (double)ld_stream(A.val + a) * (double)ld_gather(x + ld_stream(A.col + a));
-                if (PROBE) { probe_atom(probe, a, glane, tb + t); ++mine; }
-            }
-            const int key = valid ? t : INT_MAX;
-            const double sum = warp_segsum_to_head(p, key, lane);
-            const int prev = shfl_up(key, 1);
-            if (valid && (lane == 0 || prev != key)) s_acc[warp][t] += sum;
-            __syncwarp();
-        }
+          }
+        };
+        if (total >= (OffT)(GU_LONG * kWarp)) steps(std::integral_constant<int, GU>{});
+        else steps(std::integral_constant<int, 1>{});
         if (lane < tc) y[tb + lane] = (ValT)s_acc[warp][lane];
         __syncwarp();
     }
@@ -124,27 +161,32 @@ __global__ void __launch_bounds__(NT)
         s_excl[tid] = wpre + incl - cnt;
         const int64_t base = (int64_t)A.off[tb];
         __syncthreads();
-        for (OffT k0 = 0; k0 < total; k0 += NT) {
-            const OffT k = k0 + tid;
-            const bool valid = k < total;
-            int t = 0;
-            if (valid) {
+        auto steps = [&](auto uc) {
+          constexpr int U = decltype(uc)::value;
+          for (OffT k0 = 0; k0 < total; k0 += U * NT) {
+            double p[U];
+            gather_steps<ValT, U, NT>(A, x, base, k0, tid, total, p);
 #pragma unroll
-                for (int s = NT / 2; s >= 1; s >>= 1)
-                    if (t + s < tc && s_excl[t + s] <= k) t += s;
+            for (int u = 0; u < U; ++u) {
+                const OffT k = k0 + u * NT + tid;
+                const bool valid = k < total;
+                int t = 0;
+                if (valid) {
+#pragma unroll
+                    for (int s = NT / 2; s >= 1; s >>= 1)
+                        if (t + s < tc && s_excl[t + s] <= k) t += s;
+                }
+                if (PROBE && valid) { probe_atom(probe, base + k, glane, tb + t); ++mine; }
+                const int key = valid ? t : INT_MAX;
+                const double sum = warp_segsum_to_head(p[u], key, lane);
+                const int prev = shfl_up(key, 1);
+                if (valid && (lane == 0 || prev != key)) s_acc[warp][t] += sum;
+                __syncwarp();
             }
-            double p = 0.0;
-            if (valid) {
-                const int64_t a = base + k;
-                p = (double)ld_stream(A.val + a) * (double)ld_gather(x + ld_stream(A.col + a));
-                if (PROBE) { probe_atom(probe, a, glane, tb + t); ++mine; }
-            }
-            const int key = valid ? t : INT_MAX;
-            const double sum = warp_segsum_to_head(p, key, lane);
-            const int prev = shfl_up(key, 1);
-            if (valid && (lane == 0 || prev != key)) s_acc[warp][t] += sum;
-            __syncwarp();
-        }
+          }
+        };
+        if (total >= (OffT)(GU_LONG * NT)) steps(std::integral_constant<int, GU>{});
+        else steps(std::integral_constant<int, 1>{});
         __syncthreads();
         if (tid < tc) {
             double r = 0.0;

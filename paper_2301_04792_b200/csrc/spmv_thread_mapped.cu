@@ -12,6 +12,10 @@
 // accumulated), so empty rows get 0 like the reference (kernels.py:63 + _fast.py:28).
 #include "lw_common.cuh"
 
+#ifndef LW_TM_UV
+#define LW_TM_UV 4   // vectors in flight per thread on long rows
+#endif
+
 namespace lw {
 
 template <class ValT>
@@ -66,6 +70,22 @@ __device__ __forceinline__ double row_dot(const int32_t* __restrict__ col,
         while (b < e && (b & (V - 1)) != 0) {
             a0 = fma((double)__ldg(val + b), (double)ld_gather(x + __ldg(col + b)), a0);
             ++b;
+        }
+        // long rows: UV vectors per step, every load issued before the first use,
+        // so a single thread keeps UV*V gathers in flight (the thread-mapped
+        // schedule puts whole long rows on one thread)
+        constexpr int UV = LW_TM_UV;
+        if (e - b >= 8 * UV * V)   // only long rows; short rows keep the plain loop below
+        for (; b + UV * V <= e; b += UV * V) {
+            typename VT::ValV v[UV];
+            typename VT::ColV c[UV];
+#pragma unroll
+            for (int u = 0; u < UV; ++u) {
+                v[u] = __ldg(reinterpret_cast<const typename VT::ValV*>(val + b) + u);
+                c[u] = __ldg(reinterpret_cast<const typename VT::ColV*>(col + b) + u);
+            }
+#pragma unroll
+            for (int u = 0; u < UV; ++u) accum_vec<ValT>(v[u], c[u], x, a0, a1);
         }
 #pragma unroll 2
         for (; b + V <= e; b += V) {

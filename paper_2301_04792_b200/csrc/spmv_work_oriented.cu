@@ -116,7 +116,7 @@ struct WoSmem {
 // 8 consecutive col_idx / values with 32-byte loads (sm_100 .v8.b32 / .v4.b64)
 __device__ __forceinline__ void ld8_col(const int32_t* p, int32_t* c) {
     const uint64_t pol = policy_evict_first();
-    asm volatile(
+    asm(
         "ld.global.nc.L1::no_allocate.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
         : "=r"(c[0]), "=r"(c[1]), "=r"(c[2]), "=r"(c[3]), "=r"(c[4]), "=r"(c[5]), "=r"(c[6]),
           "=r"(c[7])
@@ -125,7 +125,7 @@ __device__ __forceinline__ void ld8_col(const int32_t* p, int32_t* c) {
 __device__ __forceinline__ void ld8_val(const float* p, float* v) {
     const uint64_t pol = policy_evict_first();
     uint32_t r[8];
-    asm volatile(
+    asm(
         "ld.global.nc.L1::no_allocate.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
           "=r"(r[7])
@@ -136,9 +136,9 @@ __device__ __forceinline__ void ld8_val(const float* p, float* v) {
 __device__ __forceinline__ void ld8_val(const double* p, double* v) {
     const uint64_t pol = policy_evict_first();
     unsigned long long r[8];
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.b64 {%0,%1,%2,%3}, [%4], %5;"
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.b64 {%0,%1,%2,%3}, [%4], %5;"
                  : "=l"(r[0]), "=l"(r[1]), "=l"(r[2]), "=l"(r[3]) : "l"(p), "l"(pol));
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.b64 {%0,%1,%2,%3}, [%4], %5;"
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.b64 {%0,%1,%2,%3}, [%4], %5;"
                  : "=l"(r[4]), "=l"(r[5]), "=l"(r[6]), "=l"(r[7]) : "l"(p + 4), "l"(pol));
 #pragma unroll
     for (int k = 0; k < 8; ++k) v[k] = __longlong_as_double((long long)r[k]);

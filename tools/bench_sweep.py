@@ -98,13 +98,14 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--out", default=None)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dtypes", default="float32,float64")
     args = ap.parse_args()
     hbm = peak()
     threads = oracle.default_threads()
     out = open(args.out, "a") if args.out else None
     for cfgname, label, A32, off_host in matrices(args.configs.split(",")):
         stats = lwb.row_length_stats(off_host)
-        for dtype in ("float32", "float64"):
+        for dtype in args.dtypes.split(","):
             A = A32 if dtype == "float32" else A32.astype("float64")
             x = torch.ones(A.cols, dtype=A.dtype, device=A.device)
             cold = A.algorithmic_bytes() < 256 << 20
