@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="spmv", choices=["spmv", "power"],
+                    help="spmv: one y=Ax per step (C3 headline); power: C5 power iteration")
+    ap.add_argument("--iters", type=int, default=20, help="power iterations per step (C5)")
     ap.add_argument("--items", type=int, default=0,
                     help="work_oriented items per lane (0 = library default)")
     return ap.parse_args()
@@ -168,15 +171,26 @@ def reference_arm(args):
     nnz = int(off[-1])
     x = np.ones(rows, dtype=np.float64)
     lanes = 32 * threads
+    iters = args.iters if args.mode == "power" else 1
+
+    def step():
+        if args.mode != "power":
+            oracle.spmv(off, col, val, x, "merge-path", lanes=lanes, threads=threads)
+            return
+        v = np.full(rows, 1.0 / np.sqrt(rows))
+        for _ in range(iters):
+            yv = oracle.spmv(off, col, val, v, "merge-path", lanes=lanes, threads=threads)
+            v = yv / np.linalg.norm(yv)
+
     for _ in range(args.warmup):
-        oracle.spmv(off, col, val, x, "merge-path", lanes=lanes, threads=threads)
+        step()
     times = []
     for _ in range(args.steps):
         t = time.perf_counter()
-        oracle.spmv(off, col, val, x, "merge-path", lanes=lanes, threads=threads)
+        step()
         times.append(time.perf_counter() - t)
     sec = float(np.mean(times))
-    gflops = 2.0 * nnz / sec / 1e9
+    gflops = 2.0 * nnz * iters / sec / 1e9
     sample = (f"full R-MAT scale {args.scale} matrix ({rows} rows, {nnz} nnz), merge-path, "
               f"fp64/int64, {threads} threads, {lanes} lanes, mean of {args.steps} runs")
     line = {
@@ -193,6 +207,89 @@ def reference_arm(args):
         "generation_s": round(gen_s, 2),
     }
     print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------
+def power_arm(args):
+    """C5: x <- A x / ||A x|| for --iters iterations on nnz-balanced row shards.
+    One step = the whole iteration sequence; each iteration is the shard's
+    work_oriented SpMV plus one NCCL all-gather of the uneven y shards."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2301_04792_b200 as lwb
+    from paper_2301_04792_b200.distributed import RowShard, nnz_balanced_bounds, power_iteration
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    dtype = "float32" if args.dtype == "fp32" else "float64"
+    full = lwb.generate_rmat_csr(args.scale, args.edge_factor, args.seed, dtype=dtype, device=dev)
+    n, nnz_total = full.rows, full.nnz
+    bounds = nnz_balanced_bounds(full.row_offsets.cpu().numpy(), world)
+    shard = RowShard(bounds, rank)
+    A = full.row_slice(shard.r0, shard.r1)
+    A = lwb.DeviceCsr(A.rows, A.cols, A.row_offsets.clone(), A.col_indices.clone(), A.values.clone())
+    del full
+    torch.cuda.empty_cache()
+    cfg = lwb.ExecutorConfig(schedule=lwb.ScheduleKind.MERGE_PATH)
+    y_local = torch.empty(A.rows, dtype=A.dtype, device=dev)
+    spmv_ev = []
+
+    def local_spmv(x):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        lwb.spmv(A, x, cfg, out=y_local)
+        e1.record()
+        spmv_ev.append((e0, e1))
+        return y_local
+
+    for _ in range(max(args.warmup, 3)):
+        power_iteration(local_spmv, n, shard, 2, dtype=A.dtype, device=dev)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    spmv_ev.clear()
+    with ClockSampler(local) as clocks:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(args.steps):
+            x, norms = power_iteration(local_spmv, n, shard, args.iters, dtype=A.dtype, device=dev)
+        t1.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t0.elapsed_time(t1) / args.steps
+    spmv_ms = sum(a.elapsed_time(b) for a, b in spmv_ev) / args.steps
+    if world > 1:
+        t = torch.tensor([ms, spmv_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, spmv_ms = float(t[0]), float(t[1])
+    gflops = 2.0 * nnz_total * args.iters / (ms * 1e-3) / 1e9
+    line = {
+        "metric": f"power iteration GFLOP/s ({args.iters} iters, work_oriented SpMV + NCCL y all-gather)",
+        "value": round(gflops, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32" if args.dtype == "fp32" else "f64",
+        "data": "synthetic",
+        "config": {"workload": f"rmat{args.scale}-ef{args.edge_factor}-seed{args.seed}-power{args.iters}",
+                   "rows": n, "nnz": nnz_total, "parallelism": f"rows{world}" if world > 1 else "single"},
+        "breakdown_ms": {"spmv_max_rank": round(spmv_ms, 3),
+                         "allgather_normalise": round(ms - spmv_ms, 3)},
+        "final_norm": norms[-1] if norms else None,
+        "gpu_launches": 3 * args.iters * args.steps,
+        "clocks": clocks.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 # ---------------------------------------------------------------------------------------
@@ -413,6 +510,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         reference_arm(args)
+    elif args.mode == "power":
+        power_arm(args)
     else:
         our_arm(args)
 

@@ -83,20 +83,24 @@ def power_iteration(local_spmv, n: int, shard: RowShard, iters: int, group=None,
         x = torch.full((n,), 1.0 / np.sqrt(n), dtype=dtype or torch.float32, device=device)
     else:
         x = x0
-    gathered = torch.empty(world * width, dtype=x.dtype, device=x.device)
-    send = torch.zeros(width, dtype=x.dtype, device=x.device)
+    even = all(c == width for c in counts)
+    if world > 1:
+        gathered = torch.empty(world * width, dtype=x.dtype, device=x.device)
+        send = torch.zeros(width, dtype=x.dtype, device=x.device)
     norms = []
     for k in range(iters):
         y_local = local_spmv(x)
-        send[: shard.rows].copy_(y_local)
         if world > 1:
+            send[: shard.rows].copy_(y_local)
             dist.all_gather_into_tensor(gathered, send, group=group)
-            y = torch.cat([gathered[r * width: r * width + counts[r]] for r in range(world)])
+            y = gathered if even else torch.cat(
+                [gathered[r * width: r * width + counts[r]] for r in range(world)])
         else:
-            y = send[: shard.rows].clone()
-        nrm = torch.linalg.vector_norm(y.double())
-        norms.append(float(nrm))
-        x = (y.double() / nrm).to(x.dtype) if float(nrm) > 0 else y
+            y = y_local
+        # ||y|| accumulated in fp64 on the device; no host sync inside the loop
+        nrm = torch.linalg.vector_norm(y, dtype=torch.float64)
+        norms.append(nrm)
+        x = torch.where(nrm > 0, y / nrm, y).to(x.dtype)
         if on_iter is not None:
             on_iter(k, x)
-    return x, norms
+    return x, [float(v) for v in norms]

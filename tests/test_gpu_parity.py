@@ -344,3 +344,26 @@ def test_rmat_work_oriented_matches_oracle(scale):
     xh = x.cpu().numpy().astype(np.float64)
     y_ref = oracle.spmv(off, col, val, xh, "merge-path", threads=oracle.default_threads())
     check_tol(y, off, col, val, xh, torch.float32, y_ref)
+
+
+# ---- iterated SpMV (C5 shape, one GPU) ---------------------------------------------------
+
+def test_power_iteration_single_gpu_matches_oracle():
+    from paper_2301_04792_b200.distributed import RowShard, nnz_balanced_bounds, power_iteration
+
+    dm = lwb.generate_rmat_csr(14, 16, seed=5, dtype="float64")
+    off = dm.row_offsets.cpu().numpy().astype(np.int64)
+    col = dm.col_indices.cpu().numpy().astype(np.int64)
+    val = dm.values.cpu().numpy()
+    shard = RowShard(nnz_balanced_bounds(off, 1), 0)
+    cfg = ExecutorConfig(schedule=ScheduleKind.WORK_ORIENTED)
+    x, norms = power_iteration(lambda v: lwb.spmv(dm, v, cfg), dm.rows, shard, 6,
+                               dtype=torch.float64, device="cuda")
+    xr = np.full(dm.rows, 1.0 / np.sqrt(dm.rows))
+    ref_norms = []
+    for _ in range(6):
+        yr = oracle.spmv(off, col, val, xr, "merge-path", lanes=64)
+        ref_norms.append(np.linalg.norm(yr))
+        xr = yr / ref_norms[-1]
+    np.testing.assert_allclose(norms, ref_norms, rtol=1e-10)
+    np.testing.assert_allclose(x.cpu().numpy(), xr, rtol=1e-9, atol=1e-12)
