@@ -81,15 +81,18 @@ __device__ __forceinline__ double ld_stream(const double* p) {
     return v;
 }
 // Gathered x: read-only path, L1-allocating, evict-last in L2.
+#ifndef LW_GATHER_L1
+#define LW_GATHER_L1 ""
+#endif
 __device__ __forceinline__ float ld_gather(const float* p) {
     float v;
-    LW_LDASM("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;"
+    LW_LDASM("ld.global.nc" LW_GATHER_L1 ".L2::cache_hint.f32 %0, [%1], %2;"
                  : "=f"(v) : "l"(p), "l"(policy_evict_last()));
     return v;
 }
 __device__ __forceinline__ double ld_gather(const double* p) {
     double v;
-    LW_LDASM("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;"
+    LW_LDASM("ld.global.nc" LW_GATHER_L1 ".L2::cache_hint.f64 %0, [%1], %2;"
                  : "=d"(v) : "l"(p), "l"(policy_evict_last()));
     return v;
 }
