@@ -160,6 +160,30 @@ int lw_spmv_host(int schedule, const lw_csr_t* A_host, const void* x_host, void*
                  int64_t lanes, int64_t group_size, int64_t tiles_per_block,
                  uintptr_t stream);
 
+/* ---- SpMM: C = A B, B dense row-major [cols x n], C row-major [rows x n] ---------
+ * The column loop wrapped around the SpMV body (Listing 4). Replaces
+ * kernels.spmm (kernels.py:129-175) and _fast.spmm_{thread_mapped,merge_path,
+ * group_mapped} (_fast.py:80-144): same schedules (a lane owns the same tiles and
+ * atoms as in SpMV), each atom adding val * B[col, :] to its row. A lane is a
+ * team of threads covering up to 32x16 bytes of columns; wider n is walked in
+ * slabs. B and C are device pointers; 16-byte aligned B/C with n a multiple of
+ * 4 (fp32) / 2 (fp64) take the vector path. lanes = 0 selects
+ * lw_spmm_auto_lanes(). Sums are fp64; group_mapped zeroes C and accumulates
+ * with atomics (like the reference's C += v * B[src]). */
+int lw_spmm_auto_lanes(int schedule, int64_t rows, int64_t nnz, int64_t n, int64_t group_size,
+                       int64_t tiles_per_block, int64_t* lanes_out);
+size_t lw_spmm_workspace(int schedule, int64_t rows, int64_t nnz, int64_t n, int64_t lanes,
+                         int32_t dtype);
+int lw_spmm_thread_mapped(const lw_csr_t* A, const void* B, void* C, int64_t n, int64_t lanes,
+                          uintptr_t stream);
+int lw_spmm_work_oriented(const lw_csr_t* A, const void* B, void* C, int64_t n, int64_t lanes,
+                          void* workspace, size_t workspace_bytes, uintptr_t stream);
+int lw_spmm_group_mapped(const lw_csr_t* A, const void* B, void* C, int64_t n, int64_t lanes,
+                         int64_t group_size, int64_t tiles_per_block, uintptr_t stream);
+int lw_spmm(int schedule, const lw_csr_t* A, const void* B, void* C, int64_t n, int64_t lanes,
+            int64_t group_size, int64_t tiles_per_block, void* workspace, size_t workspace_bytes,
+            uintptr_t stream);
+
 /* ---- synthetic inputs (counter-based, identical on host oracle and device) ---- */
 
 /* R-MAT edge keys: keys[i] = (row << scale) | col of edge e = edge_begin + i,

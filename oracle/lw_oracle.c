@@ -141,6 +141,103 @@ EXPORT void lwo_spmv_group_mapped(const int64_t* off, const int64_t* col, const 
     }
 }
 
+/* ---- SpMM: C = A B, B row-major [cols x n], C row-major [rows x n] ----------
+ * The column loop wraps the SpMV body (Listing 4; kernels.py:129-175). */
+
+/* _fast.py:80-90 — lane l owns tiles l, l+P, ...; per column a sequential fp64 sum */
+EXPORT void lwo_spmm_thread_mapped(const int64_t* off, const int64_t* col, const double* val,
+                                   const double* B, double* C, int64_t rows, int64_t n,
+                                   int64_t lanes, int threads) {
+#pragma omp parallel num_threads(threads)
+    {
+        const int j = omp_get_thread_num(), T = omp_get_num_threads();
+        for (int64_t lane = j; lane < lanes; lane += T)
+            for (int64_t t = lane; t < rows; t += lanes)
+                for (int64_t c = 0; c < n; ++c) {
+                    double acc = 0.0;
+                    for (int64_t a = off[t]; a < off[t + 1]; ++a) acc += val[a] * B[col[a] * n + c];
+                    C[t * n + c] = acc;
+                }
+    }
+}
+
+/* _fast.py:93-118 + kernels.py:153-163 — per-lane slices; the trailing partial
+ * row becomes a carry row of n values; carries added in lane order. */
+EXPORT int lwo_spmm_merge_path(const int64_t* off, const int64_t* col, const double* val,
+                               const double* B, double* C, int64_t rows, int64_t nnz, int64_t n,
+                               int64_t lanes, int threads) {
+    int64_t* coords = (int64_t*)malloc(sizeof(int64_t) * 2 * (lanes + 1));
+    int64_t* carry_tile = (int64_t*)malloc(sizeof(int64_t) * lanes);
+    double* carry_val = (double*)calloc((size_t)(lanes * (n > 0 ? n : 1)), sizeof(double));
+    if (!coords || !carry_tile || !carry_val) { free(coords); free(carry_tile); free(carry_val); return -1; }
+    lwo_merge_path_partition(off, rows, nnz, lanes, coords, threads);
+#pragma omp parallel num_threads(threads)
+    {
+        const int j = omp_get_thread_num(), T = omp_get_num_threads();
+        for (int64_t lane = j; lane < lanes; lane += T) {
+            const int64_t atom_begin = coords[2 * lane + 1];
+            const int64_t tile_end = coords[2 * lane + 2], atom_end = coords[2 * lane + 3];
+            int64_t atom = atom_begin;
+            for (int64_t t = coords[2 * lane]; t < tile_end; ++t) {
+                const int64_t row_end = off[t + 1];
+                for (int64_t c = 0; c < n; ++c) {
+                    double acc = 0.0;
+                    for (int64_t a = atom; a < row_end; ++a) acc += val[a] * B[col[a] * n + c];
+                    C[t * n + c] = acc;
+                }
+                atom = row_end;
+            }
+            carry_tile[lane] = -1;
+            if (atom < atom_end) {
+                carry_tile[lane] = tile_end;
+                for (int64_t c = 0; c < n; ++c) {
+                    double acc = 0.0;
+                    for (int64_t a = atom; a < atom_end; ++a) acc += val[a] * B[col[a] * n + c];
+                    carry_val[lane * n + c] = acc;
+                }
+            }
+        }
+    }
+    for (int64_t lane = 0; lane < lanes; ++lane)
+        if (carry_tile[lane] >= 0)
+            for (int64_t c = 0; c < n; ++c) C[carry_tile[lane] * n + c] += carry_val[lane * n + c];
+    free(coords);
+    free(carry_tile);
+    free(carry_val);
+    return 0;
+}
+
+/* _fast.py:121-144 — group-mapped member loop, C pre-zeroed and accumulated */
+EXPORT void lwo_spmm_group_mapped(const int64_t* off, const int64_t* col, const double* val,
+                                  const double* B, double* C, int64_t rows, int64_t n,
+                                  int64_t lanes, int64_t gs, int64_t tpb, int threads) {
+    const int64_t groups = (lanes + gs - 1) / gs;
+    const int64_t blocks = (rows + tpb - 1) / tpb;
+    memset(C, 0, sizeof(double) * (size_t)(rows * n));
+#pragma omp parallel num_threads(threads)
+    {
+        const int j = omp_get_thread_num(), T = omp_get_num_threads();
+        for (int64_t g = j; g < groups; g += T) {
+            const int64_t members = imin(gs, lanes - g * gs);
+            if (members <= 0) continue;
+            for (int64_t b = g; b < blocks; b += groups) {
+                const int64_t tb = b * tpb, tc = imin(tpb, rows - tb);
+                const int64_t base = off[tb], total = off[tb + tc] - base;
+                for (int64_t m = 0; m < members; ++m) {
+                    int64_t t = tb;
+                    for (int64_t k = m; k < total; k += members) {
+                        const int64_t a = base + k;
+                        while (off[t + 1] <= a) ++t;
+                        const double v = val[a];
+                        const double* src = B + col[a] * n;
+                        for (int64_t c = 0; c < n; ++c) C[t * n + c] += v * src[c];
+                    }
+                }
+            }
+        }
+    }
+}
+
 /* ---- assignment maps (executor.py:132-209, 224-251) ------------------------
  * For every atom: the lane that processes it and the tile it is attributed to;
  * per lane: how many atoms it processes. Arrays may be NULL. lane_atoms is

@@ -58,6 +58,10 @@ def lib():
             "lwo_spmv_thread_mapped": (None, [_p, _p, _p, _p, _p, _i64, _i64, _int]),
             "lwo_spmv_merge_path": (_int, [_p, _p, _p, _p, _p, _i64, _i64, _i64, _int, _p]),
             "lwo_spmv_group_mapped": (None, [_p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _int]),
+            "lwo_spmm_thread_mapped": (None, [_p, _p, _p, _p, _p, _i64, _i64, _i64, _int]),
+            "lwo_spmm_merge_path": (_int, [_p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _int]),
+            "lwo_spmm_group_mapped": (None, [_p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64,
+                                             _int]),
             "lwo_assign_thread_mapped": (None, [_p, _i64, _i64, _p, _p, _p]),
             "lwo_assign_merge_path": (None, [_p, _i64, _i64, _i64, _p, _p, _p]),
             "lwo_assign_group_mapped": (None, [_p, _i64, _i64, _i64, _i64, _p, _p, _p]),
@@ -168,6 +172,41 @@ def spmv(off, col, val, x, schedule: str = "merge-path", lanes: int | None = Non
     else:
         raise ValueError(schedule)
     return y
+
+
+def spmm(off, col, val, B, schedule: str = "merge-path", lanes: int | None = None,
+         threads: int = 1, group_size: int = 32, tiles_per_block: int | None = None) -> np.ndarray:
+    """fp64 C = A B (B row-major [cols, n]) under a schedule, reference lane semantics
+    (reference kernels.py:129-175, _fast.py:80-144)."""
+    off, col, B = _i64a(off), _i64a(col), _f64a(B)
+    val = _f64a(val)
+    if B.ndim != 2:
+        raise ValueError("B must be 2-D")
+    rows, nnz, n = off.size - 1, int(off[-1]), B.shape[1]
+    lanes = lanes or threads * 32
+    C = np.zeros((rows, n), dtype=np.float64)
+    L = lib()
+    if schedule == "thread-mapped":
+        L.lwo_spmm_thread_mapped(_ptr(off), _ptr(col), _ptr(val), _ptr(B), _ptr(C), rows, n, lanes,
+                                 threads)
+    elif schedule == "merge-path":
+        if L.lwo_spmm_merge_path(_ptr(off), _ptr(col), _ptr(val), _ptr(B), _ptr(C), rows, nnz, n,
+                                 lanes, threads):
+            raise MemoryError("oracle spmm allocation failed")
+    elif schedule == "group-mapped":
+        L.lwo_spmm_group_mapped(_ptr(off), _ptr(col), _ptr(val), _ptr(B), _ptr(C), rows, n, lanes,
+                                group_size, tiles_per_block or group_size, threads)
+    else:
+        raise ValueError(schedule)
+    return C
+
+
+def abs_spmm_sums(off, col, val, B) -> np.ndarray:
+    """sum_j |A_ij B_jc| per (row, column) — the tolerance scale for SpMM."""
+    off, col = _i64a(off), _i64a(col)
+    prod = np.abs(_f64a(val)[:, None] * _f64a(B)[col])
+    csum = np.concatenate([np.zeros((1, prod.shape[1])), np.cumsum(prod, axis=0)])
+    return csum[off[1:]] - csum[off[:-1]]
 
 
 def abs_row_sums(off, col, val, x) -> np.ndarray:

@@ -16,7 +16,8 @@ from .device import (DeviceCsr, device_group_plan_prefix, device_merge_path_part
 from .executor import (SENTINEL_TILE, CarryOut, CarryPolicy, ExecutorConfig, ImbalanceReport,
                        SUM_CARRIES, device_config, execute_merge_path, execute_tile_major,
                        fixup_combine, imbalance)
-from .kernels import (HeuristicConfig, choose_spmv_schedule, spmv, spmv_auto, spmv_probe)
+from .kernels import (HeuristicConfig, choose_spmv_schedule, spmm, spmv, spmv_auto,
+                      spmv_probe)
 from .schedules import (GroupMappedSchedule, GroupPlan, MergePathCoord, MergePathSchedule,
                         MergePathSlice, Schedule, ScheduleKind, ThreadMappedSchedule,
                         exclusive_prefix_sum, get_tile, group_plan, make_schedule,
@@ -41,6 +42,6 @@ __all__ = [
     "generate_rmat_csr", "get_tile", "group_plan", "imbalance", "infinite_range",
     "lane_stride_range", "make_schedule", "merge_path_partition", "merge_path_search",
     "merge_path_slices", "num_blocks", "numba_active", "rmat_thresholds", "row_length_stats",
-    "spmv", "spmv_auto", "spmv_probe", "step_range", "thread_mapped_tiles", "tile_offsets",
+    "spmm", "spmv", "spmv_auto", "spmv_probe", "step_range", "thread_mapped_tiles", "tile_offsets",
     "use_backend", "validate_csr",
 ]

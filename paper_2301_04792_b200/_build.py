@@ -28,6 +28,7 @@ SOURCES = [
     "spmv_thread_mapped.cu",
     "spmv_work_oriented.cu",
     "spmv_group_mapped.cu",
+    "spmm.cu",
     "generators.cu",
 ]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -43,6 +43,12 @@ EXPORTS = (
     "lw_spmv_workspace",
     "lw_spmv",
     "lw_spmv_host",
+    "lw_spmm_auto_lanes",
+    "lw_spmm_workspace",
+    "lw_spmm_thread_mapped",
+    "lw_spmm_work_oriented",
+    "lw_spmm_group_mapped",
+    "lw_spmm",
     "lw_rmat_keys",
     "lw_hash_values",
 )
@@ -103,6 +109,14 @@ _SIGNATURES = {
     "lw_spmv_workspace": (_sz, [ctypes.c_int, _i64, _i64, _i64, _i32]),
     "lw_spmv": (ctypes.c_int, [ctypes.c_int, _csr_p, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _up]),
     "lw_spmv_host": (ctypes.c_int, [ctypes.c_int, _csr_p, _vp, _vp, _i64, _i64, _i64, _up]),
+    "lw_spmm_auto_lanes": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _i64, _i64, _i64,
+                                          ctypes.POINTER(_i64)]),
+    "lw_spmm_workspace": (_sz, [ctypes.c_int, _i64, _i64, _i64, _i64, _i32]),
+    "lw_spmm_thread_mapped": (ctypes.c_int, [_csr_p, _vp, _vp, _i64, _i64, _up]),
+    "lw_spmm_work_oriented": (ctypes.c_int, [_csr_p, _vp, _vp, _i64, _i64, _vp, _sz, _up]),
+    "lw_spmm_group_mapped": (ctypes.c_int, [_csr_p, _vp, _vp, _i64, _i64, _i64, _i64, _up]),
+    "lw_spmm": (ctypes.c_int, [ctypes.c_int, _csr_p, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _sz,
+                               _up]),
     "lw_rmat_keys": (ctypes.c_int, [_i32, _i64, _i64, _u32, _u32, _u32, _u64, _vp, _up]),
     "lw_hash_values": (ctypes.c_int, [_vp, _i64, _u64, _i32, _vp, _up]),
 }

@@ -17,6 +17,9 @@ int merge_path_partition(int64_t, int64_t, const void*, int, int64_t, int64_t*, 
 int group_plan_prefix(int64_t, const void*, int, int64_t, int64_t*, cudaStream_t);
 int rmat_keys(int, int64_t, int64_t, uint32_t, uint32_t, uint32_t, uint64_t, int64_t*, cudaStream_t);
 int hash_values(const int64_t*, int64_t, uint64_t, int, void*, cudaStream_t);
+int spmm(int, const lw_csr_t*, const void*, void*, int64_t, int64_t, int64_t, int64_t, void*, size_t, cudaStream_t);
+int64_t spmm_auto_lanes(int schedule, int64_t rows, int64_t nnz, int64_t n, int64_t gs, int64_t tpb);
+size_t spmm_wo_workspace(int64_t lanes, int64_t n);
 
 static int g_sm[64];
 static std::mutex g_sm_mu;
@@ -230,6 +233,61 @@ int lw_spmv_host(int schedule, const lw_csr_t* H, const void* x_host, void* y_ho
     if (!rc) rc = (int)fe;
     if (!rc) rc = (int)se;
     return rc;
+}
+
+/* ---- SpMM ---------------------------------------------------------------------------- */
+
+int lw_spmm_auto_lanes(int schedule, int64_t rows, int64_t nnz, int64_t n, int64_t gs, int64_t tpb,
+                       int64_t* lanes_out) {
+    if (!lanes_out || rows < 0 || nnz < 0 || n < 0) return LW_E_INVALID_ARG;
+    if (schedule != LW_THREAD_MAPPED && schedule != LW_MERGE_PATH && schedule != LW_GROUP_MAPPED)
+        return LW_E_INVALID_ARG;
+    if (schedule == LW_GROUP_MAPPED && (gs < 1 || tpb < 1)) return LW_E_INVALID_ARG;
+    *lanes_out = spmm_auto_lanes(schedule, rows, nnz, n, gs, tpb);
+    return LW_OK;
+}
+
+size_t lw_spmm_workspace(int schedule, int64_t rows, int64_t nnz, int64_t n, int64_t lanes,
+                         int32_t dtype) {
+    (void)dtype;
+    if (schedule != LW_MERGE_PATH || rows < 0 || nnz < 0 || n < 0 || lanes < 0) return 0;
+    if (lanes == 0) lanes = spmm_auto_lanes(schedule, rows, nnz, n, 0, 0);
+    return spmm_wo_workspace(lanes, n);
+}
+
+static int spmm_entry(int schedule, const lw_csr_t* A, const void* B, void* C, int64_t n,
+                      int64_t lanes, int64_t gs, int64_t tpb, void* ws, size_t ws_bytes,
+                      uintptr_t stream) {
+    int rc = check_csr(A);
+    if (rc) return rc;
+    if (n < 0 || lanes < 0) return LW_E_INVALID_ARG;
+    if (A->rows > 0 && n > 0 && !C) return LW_E_INVALID_ARG;
+    if (A->nnz > 0 && n > 0 && !B) return LW_E_INVALID_ARG;
+    if (schedule == LW_GROUP_MAPPED && (gs < 1 || tpb < 1)) return LW_E_INVALID_ARG;
+    if (schedule != LW_THREAD_MAPPED && schedule != LW_MERGE_PATH && schedule != LW_GROUP_MAPPED)
+        return LW_E_INVALID_ARG;
+    if (lanes == 0) lanes = spmm_auto_lanes(schedule, A->rows, A->nnz, n, gs, tpb);
+    return spmm(schedule, A, B, C, n, lanes, gs, tpb, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int lw_spmm_thread_mapped(const lw_csr_t* A, const void* B, void* C, int64_t n, int64_t lanes,
+                          uintptr_t stream) {
+    return spmm_entry(LW_THREAD_MAPPED, A, B, C, n, lanes, 0, 0, nullptr, 0, stream);
+}
+
+int lw_spmm_work_oriented(const lw_csr_t* A, const void* B, void* C, int64_t n, int64_t lanes,
+                          void* ws, size_t ws_bytes, uintptr_t stream) {
+    return spmm_entry(LW_MERGE_PATH, A, B, C, n, lanes, 0, 0, ws, ws_bytes, stream);
+}
+
+int lw_spmm_group_mapped(const lw_csr_t* A, const void* B, void* C, int64_t n, int64_t lanes,
+                         int64_t gs, int64_t tpb, uintptr_t stream) {
+    return spmm_entry(LW_GROUP_MAPPED, A, B, C, n, lanes, gs, tpb, nullptr, 0, stream);
+}
+
+int lw_spmm(int schedule, const lw_csr_t* A, const void* B, void* C, int64_t n, int64_t lanes,
+            int64_t gs, int64_t tpb, void* ws, size_t ws_bytes, uintptr_t stream) {
+    return spmm_entry(schedule, A, B, C, n, lanes, gs, tpb, ws, ws_bytes, stream);
 }
 
 int lw_rmat_keys(int32_t scale, int64_t edge_begin, int64_t n_edges, uint32_t t_a, uint32_t t_ab,

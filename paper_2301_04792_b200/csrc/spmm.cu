@@ -1,0 +1,337 @@
+// spmm.cu — C = A B (B dense row-major [cols x n], C row-major [rows x n]) under
+// the three schedules. The paper's SpMM is "a loop over the columns of B wrapped
+// around the SpMV body" (Listing 4); the reference restates it as
+// kernels.spmm (kernels.py:129-175) over _fast.spmm_{thread_mapped,merge_path,
+// group_mapped} (_fast.py:80-144). The schedules -- which lane owns which tiles
+// and atoms -- are exactly the SpMV ones; only the per-atom work widens from one
+// x value to one row of B.
+//
+// Device mapping: a lane is a TEAM of TS threads (TS = power of two <= 32) that
+// covers a slab of TS*VEC consecutive columns, VEC columns per thread with one
+// 16-byte load of B / store of C (VEC = 1 when n or the pointers do not allow
+// it). Slabs wider than 32*VEC are walked one after the other, re-reading the
+// lane's atoms (the reference's column loop). A team reads each atom's column
+// index and value once (the same address for the whole team, one L1 request)
+// and gathers a contiguous TS*VEC-wide row segment of B. Sums are fp64 and follow
+// the atom order of the reference loops, so integer data is bit-exact.
+#include "lw_common.cuh"
+
+namespace lw {
+
+int mp_bound_tiles(const lw_csr_t* A, int64_t lanes, int64_t* tiles, cudaStream_t s);
+int64_t group_auto_lanes(int64_t rows, int64_t gs, int64_t tpb);
+
+constexpr int MM_NT = 256;   // threads per CTA (a multiple of every team size)
+constexpr int MM_U = 4;      // atoms per batch: col/val/B loads in flight per thread
+
+// VEC consecutive values of B / C
+template <class ValT, int VEC>
+__device__ __forceinline__ void ld_row(const ValT* p, ValT* v) {
+    if constexpr (VEC == 4) {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(p));
+        v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    } else if constexpr (VEC == 2) {
+        const double2 q = __ldg(reinterpret_cast<const double2*>(p));
+        v[0] = q.x; v[1] = q.y;
+    } else {
+        v[0] = __ldg(p);
+    }
+}
+template <class ValT, int VEC>
+__device__ __forceinline__ void st_row(ValT* p, const double* a) {
+    if constexpr (VEC == 4) {
+        *reinterpret_cast<float4*>(p) = make_float4((float)a[0], (float)a[1], (float)a[2], (float)a[3]);
+    } else if constexpr (VEC == 2) {
+        *reinterpret_cast<double2*>(p) = make_double2(a[0], a[1]);
+    } else {
+        p[0] = (ValT)a[0];
+    }
+}
+
+// Accumulate atoms [a, a+cnt) (cnt <= MM_U, all in the same row) into acc.
+template <class OffT, class ValT, int VEC>
+__device__ __forceinline__ void mm_batch(const Csr<OffT, ValT>& A, const ValT* __restrict__ B,
+                                         int64_t n, int64_t c, bool active, int64_t a, int cnt,
+                                         double* acc) {
+    int32_t col[MM_U];
+    ValT val[MM_U];
+#pragma unroll
+    for (int k = 0; k < MM_U; ++k) {
+        col[k] = k < cnt ? __ldg(A.col + a + k) : 0;
+        val[k] = k < cnt ? __ldg(A.val + a + k) : (ValT)0;
+    }
+    ValT b[MM_U][VEC];
+#pragma unroll
+    for (int k = 0; k < MM_U; ++k) {
+        if (active && k < cnt) ld_row<ValT, VEC>(B + (int64_t)col[k] * n + c, b[k]);
+        else
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) b[k][j] = (ValT)0;
+    }
+#pragma unroll
+    for (int k = 0; k < MM_U; ++k)
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) acc[j] = fma((double)val[k], (double)b[k][j], acc[j]);
+}
+
+// Full sum of atoms [s, e) for one slab (sequential in atom order).
+template <class OffT, class ValT, int VEC>
+__device__ __forceinline__ void mm_range(const Csr<OffT, ValT>& A, const ValT* __restrict__ B,
+                                         int64_t n, int64_t c, bool active, int64_t s, int64_t e,
+                                         double* acc) {
+    for (int64_t a = s; a < e; a += MM_U) {
+        const int cnt = (int)min((int64_t)MM_U, e - a);
+        mm_batch<OffT, ValT, VEC>(A, B, n, c, active, a, cnt, acc);
+    }
+}
+
+// ---- thread_mapped: lane l owns tiles l, l+P, ... (_fast.py:80-90) --------------------
+template <class OffT, class ValT, int VEC>
+__global__ void __launch_bounds__(MM_NT)
+    k_spmm_thread_mapped(Csr<OffT, ValT> A, const ValT* __restrict__ B, ValT* __restrict__ C,
+                         int64_t n, int64_t lanes, int lg_ts) {
+    const int64_t gt = (int64_t)blockIdx.x * MM_NT + threadIdx.x;
+    const int64_t lane = gt >> lg_ts;
+    const int tl = (int)(gt & ((1 << lg_ts) - 1));
+    if (lane >= lanes) return;
+    const int64_t sw = ((int64_t)VEC) << lg_ts;   // slab width
+    for (int64_t t = lane; t < A.rows; t += lanes) {
+        const int64_t s = (int64_t)__ldg(A.off + t), e = (int64_t)__ldg(A.off + t + 1);
+        for (int64_t cs = 0; cs < n; cs += sw) {
+            const int64_t c = cs + (int64_t)tl * VEC;
+            const bool active = c < n;
+            double acc[VEC];
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) acc[j] = 0.0;
+            mm_range<OffT, ValT, VEC>(A, B, n, c, active, s, e, acc);
+            if (active) st_row<ValT, VEC>(C + t * n + c, acc);
+        }
+    }
+}
+
+// ---- work_oriented (merge path): even share of rows+nnz per lane (_fast.py:93-118) ----
+// Lane k walks diagonals [min(k*items,total), min((k+1)*items,total)): rows
+// [t0, t1) end inside its slice and are assigned; the partial row t1 becomes the
+// lane's carry (n values), added in lane order by k_spmm_carry_fixup.
+template <class OffT, class ValT, int VEC>
+__global__ void __launch_bounds__(MM_NT)
+    k_spmm_work_oriented(Csr<OffT, ValT> A, const ValT* __restrict__ B, ValT* __restrict__ C,
+                         int64_t n, int64_t lanes, int64_t items, int lg_ts,
+                         const int64_t* __restrict__ bound_tile, int64_t* __restrict__ carry_tile,
+                         double* __restrict__ carry_val) {
+    const int64_t gt = (int64_t)blockIdx.x * MM_NT + threadIdx.x;
+    const int64_t lane = gt >> lg_ts;
+    const int tl = (int)(gt & ((1 << lg_ts) - 1));
+    if (lane >= lanes) return;
+    const int64_t total = A.rows + A.nnz;
+    const int64_t d0 = min(lane * items, total), d1 = min((lane + 1) * items, total);
+    const int64_t t0 = bound_tile[lane], t1 = bound_tile[lane + 1];
+    const int64_t a0 = d0 - t0, a1 = d1 - t1;
+    const int64_t sw = ((int64_t)VEC) << lg_ts;
+    // the partial row t1 covers atoms [ts, a1)
+    const int64_t ts = t1 > t0 ? (int64_t)__ldg(A.off + t1) : a0;
+    const bool carry = a1 > ts;
+    if (tl == 0) carry_tile[lane] = carry ? t1 : -1;
+    for (int64_t cs = 0; cs < n; cs += sw) {
+        const int64_t c = cs + (int64_t)tl * VEC;
+        const bool active = c < n;
+        int64_t a = a0;
+        for (int64_t t = t0; t < t1; ++t) {
+            const int64_t e = (int64_t)__ldg(A.off + t + 1);
+            double acc[VEC];
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) acc[j] = 0.0;
+            mm_range<OffT, ValT, VEC>(A, B, n, c, active, a, e, acc);
+            if (active) st_row<ValT, VEC>(C + t * n + c, acc);
+            a = e;
+        }
+        if (carry && active) {
+            double acc[VEC];
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) acc[j] = 0.0;
+            mm_range<OffT, ValT, VEC>(A, B, n, c, active, ts, a1, acc);
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) carry_val[lane * n + c + j] = acc[j];
+        }
+    }
+}
+
+// Ordered carry fix-up, one thread per (carry, column): the head of every run of
+// carries into one row sums the run in lane order and adds it (kernels.py:160-162).
+template <class ValT>
+__global__ void k_spmm_carry_fixup(const int64_t* __restrict__ carry_tile,
+                                   const double* __restrict__ carry_val, int64_t lanes, int64_t n,
+                                   ValT* __restrict__ C) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= lanes * n) return;
+    const int64_t k = i / n, c = i - k * n;
+    const int64_t r = carry_tile[k];
+    if (r < 0) return;
+    for (int64_t m = k - 1; m >= 0; --m) {
+        const int64_t t = carry_tile[m];
+        if (t == r) return;   // not the head of its run
+        if (t >= 0) break;
+    }
+    double s = 0.0;
+    for (int64_t m = k; m < lanes; ++m) {
+        const int64_t t = carry_tile[m];
+        if (t < 0) continue;
+        if (t != r) break;
+        s += carry_val[m * n + c];
+    }
+    C[r * n + c] = (ValT)((double)C[r * n + c] + s);
+}
+
+// ---- group_mapped: groups own blocks of tiles, members stride atoms (_fast.py:121-144) --
+// Lane = (group g, member m); C is zeroed first and accumulated, like the
+// reference (kernels.py:164-175 writes C += v * B[src]).
+template <class ValT>
+__device__ __forceinline__ void atomic_add_out(ValT* p, double v) {
+    atomicAdd(p, (ValT)v);
+}
+
+template <class OffT, class ValT, int VEC>
+__global__ void __launch_bounds__(MM_NT)
+    k_spmm_group_mapped(Csr<OffT, ValT> A, const ValT* __restrict__ B, ValT* __restrict__ C,
+                        int64_t n, int64_t lanes, int64_t gs, int64_t tpb, int lg_ts) {
+    const int64_t gt = (int64_t)blockIdx.x * MM_NT + threadIdx.x;
+    const int64_t lane = gt >> lg_ts;
+    const int tl = (int)(gt & ((1 << lg_ts) - 1));
+    if (lane >= lanes) return;
+    const int64_t groups = (lanes + gs - 1) / gs;
+    const int64_t g = lane / gs, m = lane - g * gs;
+    const int64_t members = min(gs, lanes - g * gs);
+    const int64_t blocks = (A.rows + tpb - 1) / tpb;
+    const int64_t sw = ((int64_t)VEC) << lg_ts;
+    for (int64_t b = g; b < blocks; b += groups) {
+        const int64_t tb = b * tpb, tc = min(tpb, A.rows - tb);
+        const int64_t base = (int64_t)__ldg(A.off + tb), tot = (int64_t)__ldg(A.off + tb + tc) - base;
+        int64_t t = tb;
+        for (int64_t k = m; k < tot; k += members) {
+            const int64_t a = base + k;
+            while ((int64_t)__ldg(A.off + t + 1) <= a) ++t;   // get_tile by monotone advance
+            const double v = (double)__ldg(A.val + a);
+            const int64_t src = __ldg(A.col + a);
+            for (int64_t cs = 0; cs < n; cs += sw) {
+                const int64_t c = cs + (int64_t)tl * VEC;
+                if (c >= n) continue;
+                ValT bv[VEC];
+                ld_row<ValT, VEC>(B + src * n + c, bv);
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) atomic_add_out(C + t * n + c + j, v * (double)bv[j]);
+            }
+        }
+    }
+}
+
+// ---- host side ------------------------------------------------------------------------
+struct MmShape {
+    int vec, lg_ts;
+};
+
+template <class ValT>
+static MmShape mm_shape(int64_t n, const void* B, const void* C) {
+    constexpr int V = 16 / (int)sizeof(ValT);
+    const bool vec = n % V == 0 && ((uintptr_t)B % 16 == 0) && ((uintptr_t)C % 16 == 0);
+    const int vw = vec ? V : 1;
+    const int64_t need = (n + vw - 1) / vw;   // threads to cover n columns
+    int lg = 0;
+    while ((1 << lg) < need && lg < 5) ++lg;
+    return MmShape{vw, lg};
+}
+
+static unsigned mm_grid(int64_t lanes, int lg_ts) {
+    return (unsigned)ceil_div((lanes << lg_ts), MM_NT);
+}
+
+int64_t mm_wo_items_target() { return 256; }
+
+int64_t spmm_auto_lanes(int schedule, int64_t rows, int64_t nnz, int64_t n, int64_t gs,
+                        int64_t tpb) {
+    int lg = 0;
+    const int64_t need = n > 0 ? (n + 3) / 4 : 1;
+    while ((1 << lg) < need && lg < 5) ++lg;
+    switch (schedule) {
+        case LW_THREAD_MAPPED: {
+            const int64_t cap = ((int64_t)sm_count() * 2048) >> lg;
+            const int64_t p = ceil_div(rows > 0 ? rows : 1, 64) * 64;
+            return p < cap ? p : cap;
+        }
+        case LW_MERGE_PATH: {
+            const int64_t total = rows + nnz;
+            const int64_t p = total > 0 ? ceil_div(total, mm_wo_items_target()) : 1;
+            return p;
+        }
+        default: return group_auto_lanes(rows, gs, tpb);
+    }
+}
+
+size_t spmm_wo_workspace(int64_t lanes, int64_t n) {
+    auto up = [](size_t b) { return (b + 255) / 256 * 256; };
+    return up((size_t)(lanes + 1) * 8) + up((size_t)lanes * 8) + up((size_t)lanes * (size_t)n * 8);
+}
+
+template <class OffT, class ValT>
+static int spmm_typed(int schedule, const lw_csr_t* H, const void* Bp, void* Cp, int64_t n,
+                      int64_t lanes, int64_t gs, int64_t tpb, void* ws, cudaStream_t s) {
+    Csr<OffT, ValT> A{H->rows, H->cols, H->nnz, (const OffT*)H->row_offsets, H->col_indices,
+                      (const ValT*)H->values};
+    const ValT* B = (const ValT*)Bp;
+    ValT* C = (ValT*)Cp;
+    const MmShape sh = mm_shape<ValT>(n, Bp, Cp);
+    const unsigned grid = mm_grid(lanes, sh.lg_ts);
+    constexpr int V = 16 / (int)sizeof(ValT);
+#define LW_MM_DISPATCH(KERN, ...)                                                      \
+    do {                                                                               \
+        if (sh.vec == V) KERN<OffT, ValT, V><<<grid, MM_NT, 0, s>>>(__VA_ARGS__);      \
+        else KERN<OffT, ValT, 1><<<grid, MM_NT, 0, s>>>(__VA_ARGS__);                  \
+    } while (0)
+    switch (schedule) {
+        case LW_THREAD_MAPPED:
+            LW_MM_DISPATCH(k_spmm_thread_mapped, A, B, C, n, lanes, sh.lg_ts);
+            LW_LAUNCH_CHECK();
+            return LW_OK;
+        case LW_MERGE_PATH: {
+            auto up = [](size_t b) { return (b + 255) / 256 * 256; };
+            unsigned char* w = (unsigned char*)ws;
+            int64_t* tiles = (int64_t*)w;
+            int64_t* c_tile = (int64_t*)(w + up((size_t)(lanes + 1) * 8));
+            double* c_val = (double*)(w + up((size_t)(lanes + 1) * 8) + up((size_t)lanes * 8));
+            const int64_t total = A.rows + A.nnz;
+            const int64_t items = total > 0 ? ceil_div(total, lanes) : 0;
+            int rc = mp_bound_tiles(H, lanes, tiles, s);
+            if (rc) return rc;
+            LW_MM_DISPATCH(k_spmm_work_oriented, A, B, C, n, lanes, items, sh.lg_ts, tiles, c_tile,
+                           c_val);
+            LW_LAUNCH_CHECK();
+            const int64_t work = lanes * n;
+            k_spmm_carry_fixup<ValT><<<(unsigned)ceil_div(work, 256), 256, 0, s>>>(c_tile, c_val,
+                                                                                  lanes, n, C);
+            LW_LAUNCH_CHECK();
+            return LW_OK;
+        }
+        case LW_GROUP_MAPPED:
+            LW_TRY(cudaMemsetAsync(C, 0, (size_t)A.rows * (size_t)n * sizeof(ValT), s));
+            LW_MM_DISPATCH(k_spmm_group_mapped, A, B, C, n, lanes, gs, tpb, sh.lg_ts);
+            LW_LAUNCH_CHECK();
+            return LW_OK;
+        default: return LW_E_INVALID_ARG;
+    }
+#undef LW_MM_DISPATCH
+}
+
+int spmm(int schedule, const lw_csr_t* A, const void* B, void* C, int64_t n, int64_t lanes,
+         int64_t gs, int64_t tpb, void* ws, size_t ws_bytes, cudaStream_t s) {
+    if (A->rows == 0 || n == 0) return LW_OK;
+    if (schedule == LW_MERGE_PATH && (!ws || ws_bytes < spmm_wo_workspace(lanes, n)))
+        return LW_E_WORKSPACE;
+    if (lanes < 1 || ceil_div(lanes << 5, MM_NT) > 0x7fffffffLL) return LW_E_UNSUPPORTED;
+    const bool o32 = A->offset_bits == 32;
+    if (A->dtype == LW_F32)
+        return o32 ? spmm_typed<int32_t, float>(schedule, A, B, C, n, lanes, gs, tpb, ws, s)
+                   : spmm_typed<int64_t, float>(schedule, A, B, C, n, lanes, gs, tpb, ws, s);
+    return o32 ? spmm_typed<int32_t, double>(schedule, A, B, C, n, lanes, gs, tpb, ws, s)
+               : spmm_typed<int64_t, double>(schedule, A, B, C, n, lanes, gs, tpb, ws, s);
+}
+
+}  // namespace lw

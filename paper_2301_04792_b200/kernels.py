@@ -23,8 +23,8 @@ from .device import DeviceCsr, Probe, Workspace, current_stream
 from .executor import ExecutorConfig
 from .schedules import ScheduleKind
 
-__all__ = ["spmv", "spmv_probe", "spmv_auto", "choose_spmv_schedule", "HeuristicConfig",
-           "schedule_code"]
+__all__ = ["spmv", "spmm", "spmv_probe", "spmv_auto", "choose_spmv_schedule",
+           "HeuristicConfig", "schedule_code"]
 
 _WS = Workspace()
 
@@ -94,6 +94,58 @@ def spmv(m, x, cfg: ExecutorConfig | None = None, *, out=None, dtype=None):
     y = torch.empty(dm.rows, dtype=dm.dtype, device=dm.device)
     _launch(dm, xd, y, cfg, None, current_stream(dm.device))
     return y.to(torch.float64).cpu().numpy()
+
+
+def _launch_spmm(m: DeviceCsr, B, C, cfg: ExecutorConfig, stream: int) -> None:
+    lib = _lib.load()
+    A = m.c_struct()
+    n = int(B.shape[1])
+    code = schedule_code(cfg.schedule)
+    lanes = _lanes_arg(cfg)
+    bp = B.data_ptr() if B.numel() else None
+    cp = C.data_ptr() if C.numel() else None
+    need = lib.lw_spmm_workspace(code, m.rows, m.nnz, n, lanes, A.dtype)
+    ws = _WS.get(need, m.device) if need else None
+    rc = lib.lw_spmm(code, A, bp, cp, n, lanes, cfg.group_size, cfg.tiles_per_block,
+                     ws.data_ptr() if ws is not None else None, need, stream)
+    _lib.check(rc, f"spmm[{cfg.schedule.value}]")
+
+
+def spmm(m, B, cfg: ExecutorConfig | None = None, *, out=None, dtype=None):
+    """C = m @ B for a dense row-major B (reference kernels.py:129-175).
+
+    Host operands (CsrMatrix + array-like B): B is validated like the reference
+    (2-D with B.shape[0] == m.cols, else ValueError), computed on the device in
+    fp64 by default and returned as a NumPy float64 [rows, k] array. Device
+    operands (DeviceCsr + torch CUDA B [cols, k] in the matrix dtype): C stays on
+    the device. The schedule assigns tiles and atoms to lanes exactly as spmv does.
+    """
+    cfg = cfg or ExecutorConfig()
+    _backend.require_cuda()
+    import torch
+
+    if isinstance(m, DeviceCsr):
+        if not isinstance(B, torch.Tensor):
+            raise TypeError("a DeviceCsr needs B as a torch CUDA tensor")
+        if B.ndim != 2 or B.shape[0] != m.cols:
+            raise ValueError(f"B has shape {tuple(B.shape)}, expected ({m.cols}, k)")
+        if B.device != m.device or B.dtype != m.dtype:
+            raise ValueError("B must be on the matrix's device with the matrix dtype")
+        B = B.contiguous()
+        C = out if out is not None else torch.empty((m.rows, B.shape[1]), dtype=m.dtype,
+                                                    device=m.device)
+        if C.shape != (m.rows, B.shape[1]) or C.dtype != m.dtype or not C.is_contiguous():
+            raise ValueError("out must be a contiguous [rows, k] tensor with the matrix dtype")
+        _launch_spmm(m, B, C, cfg, current_stream(m.device))
+        return C
+    Bh = np.ascontiguousarray(B, dtype=np.float64)
+    if Bh.ndim != 2 or Bh.shape[0] != m.cols:
+        raise ValueError(f"B has shape {Bh.shape}, expected ({m.cols}, k)")
+    dm = DeviceCsr.from_host(m, dtype=dtype or "float64")
+    Bd = torch.from_numpy(Bh).to(dm.device).to(dm.dtype)
+    C = torch.empty((dm.rows, Bh.shape[1]), dtype=dm.dtype, device=dm.device)
+    _launch_spmm(dm, Bd, C, cfg, current_stream(dm.device))
+    return C.to(torch.float64).cpu().numpy()
 
 
 def spmv_probe(m: DeviceCsr, x, cfg: ExecutorConfig | None = None):

@@ -43,6 +43,15 @@ class Golden:
                    unpack(g["val"], g["col_idx"], k), unpack(g["x"], g["x_idx"], k),
                    int(g["rows"][k]), int(g["cols"][k]))
 
+    def spmm_cases(self):
+        """Yield (k, off, col, val, B, rows, cols) for every golden SpMM matrix."""
+        g = self["spmm"]
+        for k in range(len(g["rows"])):
+            n = int(g["n"][k])
+            yield (k, unpack(g["off"], g["off_idx"], k), unpack(g["col"], g["col_idx"], k),
+                   unpack(g["val"], g["col_idx"], k), unpack(g["B"], g["B_idx"], k).reshape(-1, n),
+                   int(g["rows"][k]), int(g["cols"][k]))
+
 
 @pytest.fixture(scope="session")
 def golden():

@@ -164,6 +164,49 @@ def make_spmv():
     )
 
 
+def make_spmm():
+    """spmm outputs (numba backend) for seeded matrices x dense B (kernels.py:129-175)."""
+    rng = np.random.default_rng(2025)
+    mats, bs, cs, meta = [], [], [], []
+    cfgs = []
+    for lanes in (5, 16, 64):
+        cfgs.append(("thread-mapped", lanes, 32, 32))
+        cfgs.append(("merge-path", lanes, 32, 32))
+        for gs in (4, 32):
+            cfgs.append(("group-mapped", lanes, gs, gs))
+    for i in range(16):
+        rows = int(rng.integers(1, 90))
+        cols = int(rng.integers(1, 90))
+        nnz = int(rng.integers(0, min(rows * cols, 700) + 1))
+        m = lw.generate_random_csr(rows, cols, nnz, seed=int(rng.integers(1 << 30)))
+        n = [1, 2, 3, 4, 8, 5, 16, 33][i % 8]
+        integer = i % 2 == 0
+        if integer:
+            m.values = rng.integers(-4, 5, size=m.nnz).astype(np.float64)
+            B = rng.integers(-3, 4, size=(cols, n)).astype(np.float64)
+        else:
+            B = rng.random((cols, n))
+        for ci, (kind, lanes, gs, tpb) in enumerate(cfgs):
+            cfg = lw.ExecutorConfig(schedule=lw.ScheduleKind(kind), lanes=lanes, worker_threads=2,
+                                    group_size=gs, tiles_per_block=tpb)
+            cs.append(lw.spmm(m, B, cfg))
+            meta.append([i, ci, int(integer)])
+        mats.append(m)
+        bs.append(B)
+    np.savez_compressed(
+        OUT / "spmm.npz",
+        rows=np.array([m.rows for m in mats]), cols=np.array([m.cols for m in mats]),
+        n=np.array([b.shape[1] for b in bs]),
+        off=pack([m.row_offsets for m in mats])[0], off_idx=pack([m.row_offsets for m in mats])[1],
+        col=pack([m.col_indices for m in mats])[0], col_idx=pack([m.col_indices for m in mats])[1],
+        val=pack([m.values for m in mats])[0],
+        B=pack(bs)[0], B_idx=pack(bs)[1],
+        C=pack(cs)[0], C_idx=pack(cs)[1], meta=np.array(meta),
+        cfg_kind=np.array([c[0] for c in cfgs]), cfg_lanes=np.array([c[1] for c in cfgs]),
+        cfg_gs=np.array([c[2] for c in cfgs]), cfg_tpb=np.array([c[3] for c in cfgs]),
+    )
+
+
 def make_generators():
     out = {}
     cases = [("random", (40, 30, 200, 1)), ("random", (300, 200, 5000, 7)),
@@ -183,8 +226,9 @@ def make_generators():
 
 if __name__ == "__main__":
     print("reference:", lw.__file__, "backend:", lw.backend_name())
-    make_schedules()
-    make_spmv()
-    make_generators()
+    which = set(sys.argv[1:]) or {"schedules", "spmv", "spmm", "generators"}
+    for name in ("schedules", "spmv", "spmm", "generators"):
+        if name in which:
+            globals()[f"make_{name}"]()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)

@@ -99,3 +99,33 @@ def test_abs_row_sums_and_tolerance():
     np.testing.assert_array_equal(s, [5.0, 6.0])
     assert oracle.tolerance_ok([1.0], np.array([1.0 + 1e-6]), [1.0], 1e-5)[0]
     assert not oracle.tolerance_ok([1.0], np.array([1.0 + 1e-4]), [1.0], 1e-5)[0]
+
+
+@pytest.mark.parametrize("threads", [1, 3])
+def test_spmm_matches_reference(golden, threads):
+    """C oracle SpMM vs lanework.spmm (numba) on every golden case (kernels.py:129-175)."""
+    g = golden["spmm"]
+    cases = list(golden.spmm_cases())
+    for ck, (mi, ci, integer) in enumerate(g["meta"]):
+        _, off, col, val, B, rows, cols = cases[mi]
+        C = oracle.spmm(off, col, val, B, str(g["cfg_kind"][ci]), lanes=int(g["cfg_lanes"][ci]),
+                        threads=threads, group_size=int(g["cfg_gs"][ci]),
+                        tiles_per_block=int(g["cfg_tpb"][ci]))
+        want = unpack(g["C"], g["C_idx"], ck).reshape(rows, B.shape[1])
+        if integer:
+            np.testing.assert_array_equal(C, want)
+        else:
+            assert oracle.tolerance_ok(C, want, oracle.abs_spmm_sums(off, col, val, B), 1e-12)[0]
+
+
+def test_spmm_column_slices_equal_spmv():
+    """column c of spmm(m, B) equals spmv(m, B[:, c]) exactly (integer data)."""
+    rng = np.random.default_rng(5)
+    off = np.concatenate([[0], np.cumsum(rng.integers(0, 9, size=40))])
+    col = rng.integers(0, 30, size=int(off[-1]))
+    val = rng.integers(-4, 5, size=col.size).astype(np.float64)
+    B = rng.integers(-3, 4, size=(30, 6)).astype(np.float64)
+    for kind in KIND_NAMES:
+        C = oracle.spmm(off, col, val, B, kind, lanes=7)
+        for c in range(6):
+            np.testing.assert_array_equal(C[:, c], oracle.spmv(off, col, val, B[:, c], kind, lanes=7))
