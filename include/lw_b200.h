@@ -38,6 +38,7 @@ extern "C" {
 #define LW_E_UNSUPPORTED 10002   /* config the device kernels do not implement       */
 #define LW_E_WORKSPACE 10003     /* workspace pointer NULL or smaller than required  */
 #define LW_E_NO_DEVICE 10004     /* no CUDA device visible                           */
+#define LW_E_FORMAT 10005        /* malformed input file: reference MatrixMarketError */
 
 /* value dtypes */
 #define LW_F32 0
@@ -183,6 +184,36 @@ int lw_spmm_group_mapped(const lw_csr_t* A, const void* B, void* C, int64_t n, i
 int lw_spmm(int schedule, const lw_csr_t* A, const void* B, void* C, int64_t n, int64_t lanes,
             int64_t group_size, int64_t tiles_per_block, void* workspace, size_t workspace_bytes,
             uintptr_t stream);
+
+/* ---- ingestion (host-native; the input side of the path) ---------------------
+ * Matrix Market coordinate text -> COO -> CSR. Replaces mmio.parse_matrix_market
+ * (mmio.py:24-107) and sparse.coo_to_csr (sparse.py:130-150). Buffers are HOST
+ * memory. Parsing is multi-threaded over line-aligned chunks; accepted syntax,
+ * error precedence (first bad line in file order) and messages follow mmio.py,
+ * returned as LW_E_FORMAT with the text in err[errlen]. */
+typedef struct lw_mm_header {
+    int64_t rows;
+    int64_t cols;
+    int64_t entries;     /* declared entry count */
+    int32_t field;       /* 0 real, 1 integer, 2 pattern */
+    int32_t symmetric;   /* 0 general, 1 symmetric (mirrored entries appended) */
+    int64_t data_offset; /* byte offset of the first line after the size header */
+} lw_mm_header_t;
+
+int lw_mm_parse_header(const char* buf, size_t len, lw_mm_header_t* header, char* err,
+                       size_t errlen);
+/* row/col/val hold capacity >= entries (x2 when symmetric) entries; *count_out
+ * receives the COO entry count (stored + mirrored off-diagonal). threads <= 0:
+ * all hardware threads. Indices are 0-based, pattern values 1.0. */
+int lw_mm_parse_entries(const char* buf, size_t len, const lw_mm_header_t* header, int64_t* row,
+                        int64_t* col, double* val, int64_t capacity, int64_t* count_out,
+                        int32_t threads, char* err, size_t errlen);
+/* Sort by (row, col), sum duplicates in input order (as np.bincount does),
+ * pack CSR: row_offsets[rows+1], col_out/val_out[>= n]; *nnz_out distinct
+ * pairs. LW_E_INVALID_ARG on an out-of-bounds entry. */
+int lw_coo_to_csr_host(int64_t rows, int64_t cols, int64_t n, const int64_t* row,
+                       const int64_t* col, const double* val, int64_t* row_offsets,
+                       int64_t* col_out, double* val_out, int64_t* nnz_out, int32_t threads);
 
 /* ---- synthetic inputs (counter-based, identical on host oracle and device) ---- */
 

@@ -23,15 +23,20 @@ from .schedules import (GroupMappedSchedule, GroupPlan, MergePathCoord, MergePat
                         exclusive_prefix_sum, get_tile, group_plan, make_schedule,
                         merge_path_partition, merge_path_search, merge_path_slices, num_blocks,
                         thread_mapped_tiles)
-from .sparse import (CsrMatrix, generate_banded_csr, generate_power_law_csr, generate_random_csr,
-                     rmat_thresholds, row_length_stats, validate_csr)
+from .mmio import (MatrixMarketError, load_matrix_market, parse_matrix_market,
+                   write_matrix_market)
+from .sparse import (CooMatrix, CsrMatrix, Graph, coo_to_csr, csr_to_coo, generate_banded_csr,
+                     generate_power_law_csr, generate_random_csr, rmat_thresholds,
+                     row_length_stats, transpose_csr, validate_coo, validate_csr)
 from .work import (TileSet, csr_tile_set, infinite_range, lane_stride_range, step_range,
                    tile_offsets)
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "BackendUnavailable", "CarryOut", "CarryPolicy", "CsrMatrix", "DeviceCsr", "ENV_VAR",
+    "BackendUnavailable", "CarryOut", "CarryPolicy", "CooMatrix", "CsrMatrix", "Graph",
+    "MatrixMarketError", "coo_to_csr", "csr_to_coo", "load_matrix_market", "parse_matrix_market",
+    "transpose_csr", "validate_coo", "write_matrix_market", "DeviceCsr", "ENV_VAR",
     "ExecutorConfig", "GroupMappedSchedule", "GroupPlan", "HeuristicConfig", "ImbalanceReport",
     "MergePathCoord", "MergePathSchedule", "MergePathSlice", "SENTINEL_TILE", "SUM_CARRIES",
     "Schedule", "ScheduleKind", "ThreadMappedSchedule", "TileSet", "backend_name",

@@ -30,6 +30,7 @@ SOURCES = [
     "spmv_group_mapped.cu",
     "spmm.cu",
     "generators.cu",
+    "mmio.cpp",
 ]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",

@@ -19,6 +19,7 @@ LW_E_INVALID_ARG = 10001
 LW_E_UNSUPPORTED = 10002
 LW_E_WORKSPACE = 10003
 LW_E_NO_DEVICE = 10004
+LW_E_FORMAT = 10005
 
 LW_F32 = 0
 LW_F64 = 1
@@ -49,6 +50,9 @@ EXPORTS = (
     "lw_spmm_work_oriented",
     "lw_spmm_group_mapped",
     "lw_spmm",
+    "lw_mm_parse_header",
+    "lw_mm_parse_entries",
+    "lw_coo_to_csr_host",
     "lw_rmat_keys",
     "lw_hash_values",
 )
@@ -77,6 +81,17 @@ class LwProbe(ctypes.Structure):
         ("atom_lane", ctypes.c_void_p),
         ("atom_tile", ctypes.c_void_p),
         ("atom_visits", ctypes.c_void_p),
+    ]
+
+
+class LwMmHeader(ctypes.Structure):
+    _fields_ = [
+        ("rows", ctypes.c_int64),
+        ("cols", ctypes.c_int64),
+        ("entries", ctypes.c_int64),
+        ("field", ctypes.c_int32),
+        ("symmetric", ctypes.c_int32),
+        ("data_offset", ctypes.c_int64),
     ]
 
 
@@ -117,6 +132,13 @@ _SIGNATURES = {
     "lw_spmm_group_mapped": (ctypes.c_int, [_csr_p, _vp, _vp, _i64, _i64, _i64, _i64, _up]),
     "lw_spmm": (ctypes.c_int, [ctypes.c_int, _csr_p, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _sz,
                                _up]),
+    "lw_mm_parse_header": (ctypes.c_int, [ctypes.c_char_p, _sz, ctypes.POINTER(LwMmHeader),
+                                          ctypes.c_char_p, _sz]),
+    "lw_mm_parse_entries": (ctypes.c_int, [ctypes.c_char_p, _sz, ctypes.POINTER(LwMmHeader), _vp,
+                                           _vp, _vp, _i64, ctypes.POINTER(_i64), _i32,
+                                           ctypes.c_char_p, _sz]),
+    "lw_coo_to_csr_host": (ctypes.c_int, [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp,
+                                          ctypes.POINTER(_i64), _i32]),
     "lw_rmat_keys": (ctypes.c_int, [_i32, _i64, _i64, _u32, _u32, _u32, _u64, _vp, _up]),
     "lw_hash_values": (ctypes.c_int, [_vp, _i64, _u64, _i32, _vp, _up]),
 }

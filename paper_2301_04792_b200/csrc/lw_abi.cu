@@ -81,6 +81,7 @@ const char* lw_error_string(int code) {
         case LW_E_UNSUPPORTED: return "configuration not supported by the device kernels";
         case LW_E_WORKSPACE: return "workspace missing or smaller than required";
         case LW_E_NO_DEVICE: return "no CUDA device visible";
+        case LW_E_FORMAT: return "malformed input file";
         default: return cudaGetErrorString((cudaError_t)code);
     }
 }

@@ -23,7 +23,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
-__all__ = ["CsrMatrix", "validate_csr", "generate_random_csr", "generate_power_law_csr",
+__all__ = ["CooMatrix", "CsrMatrix", "Graph", "validate_coo", "validate_csr", "coo_to_csr",
+           "csr_to_coo", "transpose_csr", "generate_random_csr", "generate_power_law_csr",
            "generate_banded_csr", "rmat_thresholds", "hash_values_np", "row_length_stats"]
 
 MASK64 = (1 << 64) - 1
@@ -64,6 +65,104 @@ class CsrMatrix:
         from .device import DeviceCsr
 
         return DeviceCsr.from_host(self, dtype=dtype, device=device, offset_bits=offset_bits)
+
+
+@dataclass
+class CooMatrix:
+    """Coordinate-format matrix; entries may be unsorted and may repeat (reference
+    sparse.py:14-37)."""
+
+    rows: int
+    cols: int
+    row: np.ndarray
+    col: np.ndarray
+    data: np.ndarray
+
+    def __post_init__(self):
+        self.row = np.asarray(self.row, dtype=np.int64)
+        self.col = np.asarray(self.col, dtype=np.int64)
+        self.data = np.asarray(self.data, dtype=np.float64)
+        if not (self.row.shape == self.col.shape == self.data.shape):
+            raise ValueError("row, col and data must have equal length")
+
+    @property
+    def nnz(self) -> int:
+        return self.row.size
+
+    def entries(self):
+        """Iterate (row, col, value) tuples; mainly for small-matrix tests."""
+        return zip(self.row.tolist(), self.col.tolist(), self.data.tolist())
+
+
+def validate_coo(m: CooMatrix) -> None:
+    """Raise ValueError if any entry lies outside the declared shape (sparse.py:74-81)."""
+    if m.rows < 0 or m.cols < 0:
+        raise ValueError("negative dimensions")
+    if m.nnz and (int(m.row.min()) < 0 or int(m.row.max()) >= m.rows or int(m.col.min()) < 0
+                  or int(m.col.max()) >= m.cols):
+        raise ValueError("entry index out of bounds")
+
+
+def coo_to_csr(coo: CooMatrix, threads: int = 0) -> CsrMatrix:
+    """Sort entries by (row, col), sum duplicates, pack CSR (reference sparse.py:130-150).
+
+    Runs in the native library (lw_coo_to_csr_host: multi-threaded sort, then
+    duplicates summed in input order, exactly as lexsort + bincount do)."""
+    import ctypes
+
+    from . import _lib
+
+    validate_coo(coo)
+    n = coo.nnz
+    row = np.ascontiguousarray(coo.row, dtype=np.int64)
+    col = np.ascontiguousarray(coo.col, dtype=np.int64)
+    data = np.ascontiguousarray(coo.data, dtype=np.float64)
+    off = np.zeros(coo.rows + 1, dtype=np.int64)
+    col_out = np.empty(n, dtype=np.int64)
+    val_out = np.empty(n, dtype=np.float64)
+    nnz = ctypes.c_int64(0)
+
+    def ptr(a):
+        return a.ctypes.data if a.size else None
+
+    rc = _lib.load().lw_coo_to_csr_host(coo.rows, coo.cols, n, ptr(row), ptr(col), ptr(data),
+                                        ptr(off), ptr(col_out), ptr(val_out), ctypes.byref(nnz),
+                                        threads)
+    _lib.check(rc, "coo_to_csr")
+    return CsrMatrix(coo.rows, coo.cols, off, col_out[:nnz.value], val_out[:nnz.value])
+
+
+def csr_to_coo(m: CsrMatrix) -> CooMatrix:
+    row = np.repeat(np.arange(m.rows), m.row_lengths())
+    return CooMatrix(m.rows, m.cols, row, m.col_indices.copy(), m.values.copy())
+
+
+def transpose_csr(m: CsrMatrix) -> CsrMatrix:
+    """Transpose via COO; the load-time answer to column-compressed inputs."""
+    coo = csr_to_coo(m)
+    return coo_to_csr(CooMatrix(m.cols, m.rows, coo.col, coo.row, coo.data))
+
+
+class Graph:
+    """A square CSR matrix read as adjacency (reference sparse.py:106-127): row =
+    source vertex, nonzero = out-edge, column = neighbour, value = edge weight.
+    Negative weights are rejected so shortest-path kernels can assume
+    non-negativity."""
+
+    def __init__(self, csr: CsrMatrix):
+        if csr.rows != csr.cols:
+            raise ValueError("adjacency matrix must be square")
+        if csr.nnz and float(csr.values.min()) < 0:
+            raise ValueError("edge weights must be non-negative")
+        self.csr = csr
+
+    @property
+    def num_vertices(self) -> int:
+        return self.csr.rows
+
+    @property
+    def num_edges(self) -> int:
+        return self.csr.nnz
 
 
 def validate_csr(m: CsrMatrix) -> None:

@@ -207,6 +207,99 @@ def make_spmm():
     )
 
 
+def _mm_text(rng, k):
+    """A Matrix Market text with the variety real files have: every field and
+    symmetry, comments and blank lines, ragged whitespace, CRLF, duplicates,
+    unsorted entries, exponents."""
+    field = ["real", "integer", "pattern"][k % 3]
+    sym = "symmetric" if k % 4 == 1 else "general"
+    rows = int(rng.integers(1, 40))
+    cols = rows if sym == "symmetric" else int(rng.integers(1, 40))
+    n = int(rng.integers(0, 3 * max(rows, cols) + 1))
+    lines = [f"%%MatrixMarket {'Matrix' if k % 5 == 0 else 'matrix'} coordinate {field} {sym}"]
+    if k % 3 == 0:
+        lines += ["% generated", ""]
+    lines.append(f"{rows} {cols} {n}")
+    for e in range(n):
+        i = int(rng.integers(1, rows + 1))
+        j = int(rng.integers(1, cols + 1))
+        if sym == "symmetric" and j > i:
+            i, j = j, i
+        sep = "\t" if (e + k) % 7 == 0 else " " * int(rng.integers(1, 3))
+        if field == "pattern":
+            lines.append(f"{i}{sep}{j}")
+        elif field == "integer":
+            lines.append(f"{i}{sep}{j}{sep}{int(rng.integers(-9, 10))}")
+        else:
+            v = float(rng.normal()) * 10.0 ** int(rng.integers(-5, 6))
+            lines.append(f"{i}{sep}{j}{sep}{v!r}" if e % 3 else f"{i} {j} {v:.6e}")
+        if e % 11 == 5:
+            lines.append("% interleaved comment")
+    nl = "\r\n" if k % 6 == 2 else "\n"
+    return nl.join(lines) + nl
+
+
+MM_ERROR_TEXTS = [
+    "",
+    "%%NotMatrixMarket matrix coordinate real general\n1 1 0\n",
+    "%%MatrixMarket matrix coordinate real\n1 1 0\n",
+    "%%MatrixMarket tensor coordinate real general\n1 1 0\n",
+    "%%MatrixMarket matrix array real general\n1 1\n",
+    "%%MatrixMarket matrix coordinate complex general\n1 1 1\n1 1 1 0\n",
+    "%%MatrixMarket matrix coordinate real hermitian\n1 1 1\n1 1 1\n",
+    "%%MatrixMarket matrix coordinate real skew-symmetric\n1 1 1\n1 1 1\n",
+    "%%MatrixMarket matrix coordinate real general\n1 1\n",
+    "%%MatrixMarket matrix coordinate real general\n% only comments\n",
+    "%%MatrixMarket matrix coordinate real general\n2 -2 1\n",
+    "%%MatrixMarket matrix coordinate real general\n2 x 1\n",
+    "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1.0\n",
+    "%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1 1.0\n2 2 2.0\n",
+    "%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1 1.0\nx y z\n",
+    "%%MatrixMarket matrix coordinate real general\n2 2 1\n3 1 1.0\n",
+    "%%MatrixMarket matrix coordinate real general\n2 2 1\n1 0 1.0\n",
+    "%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1\n",
+    "%%MatrixMarket matrix coordinate real general\n2 2 1\nx y z\n",
+    "%%MatrixMarket matrix coordinate pattern general\n2 2 1\n1 1 1\n",
+    "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1.0\n1 2 abc\n",
+    "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 5 1.0\n1 x 1\n",
+    "%%MatrixMarket matrix coordinate integer general\n3 3 1\n1.5 1 2\n",
+    "%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1 0x10\n",
+]
+
+
+def make_mmio():
+    """parse_matrix_market + coo_to_csr outputs, and the error message of every
+    malformed text (mmio.py:24-107, sparse.py:130-150)."""
+    from lanework.mmio import MatrixMarketError
+
+    rng = np.random.default_rng(77)
+    texts, coo_r, coo_c, coo_v, shapes, offs, cols_, vals_ = [], [], [], [], [], [], [], []
+    for k in range(36):
+        t = _mm_text(rng, k)
+        coo = lw.parse_matrix_market(t)
+        csr = lw.coo_to_csr(coo)
+        texts.append(t)
+        coo_r.append(coo.row)
+        coo_c.append(coo.col)
+        coo_v.append(coo.data)
+        shapes.append([coo.rows, coo.cols])
+        offs.append(csr.row_offsets)
+        cols_.append(csr.col_indices)
+        vals_.append(csr.values)
+    msgs = []
+    for t in MM_ERROR_TEXTS:
+        try:
+            lw.parse_matrix_market(t)
+            msgs.append("")
+        except MatrixMarketError as exc:
+            msgs.append(str(exc))
+    np.savez_compressed(
+        OUT / "mmio.npz", texts=np.array(texts), shapes=np.array(shapes),
+        coo_r=pack(coo_r)[0], coo_c=pack(coo_c)[0], coo_v=pack(coo_v)[0], coo_idx=pack(coo_r)[1],
+        off=pack(offs)[0], off_idx=pack(offs)[1], col=pack(cols_)[0], val=pack(vals_)[0],
+        col_idx=pack(cols_)[1], err_texts=np.array(MM_ERROR_TEXTS), err_msgs=np.array(msgs))
+
+
 def make_generators():
     out = {}
     cases = [("random", (40, 30, 200, 1)), ("random", (300, 200, 5000, 7)),
@@ -226,8 +319,8 @@ def make_generators():
 
 if __name__ == "__main__":
     print("reference:", lw.__file__, "backend:", lw.backend_name())
-    which = set(sys.argv[1:]) or {"schedules", "spmv", "spmm", "generators"}
-    for name in ("schedules", "spmv", "spmm", "generators"):
+    which = set(sys.argv[1:]) or {"schedules", "spmv", "spmm", "mmio", "generators"}
+    for name in ("schedules", "spmv", "spmm", "mmio", "generators"):
         if name in which:
             globals()[f"make_{name}"]()
     for f in sorted(OUT.glob("*.npz")):
