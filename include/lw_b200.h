@@ -185,6 +185,37 @@ int lw_spmm(int schedule, const lw_csr_t* A, const void* B, void* C, int64_t n, 
             int64_t group_size, int64_t tiles_per_block, void* workspace, size_t workspace_bytes,
             uintptr_t stream);
 
+/* ---- SSSP / BFS: frontier relaxation under the three schedules ---------------
+ * Replaces kernels.sssp / sssp_pass / bfs (kernels.py:230-381) and the numba
+ * relax loops (_fast.py:147-170); the paper's Listing 5. G is a square CSR
+ * (row = source vertex, value = non-negative edge weight, fp32 or fp64). A pass
+ * takes the compacted frontier active[n_active] (vertex ids in increasing order,
+ * = np.flatnonzero(in_frontier)), builds the frontier tile set (tiles = active
+ * vertices, atoms = out-edges) on the device and relaxes every atom under the
+ * schedule: SSSP by atomicMin on the fp64 bit pattern of dist (out[v] = 1 when
+ * the distance strictly improved), BFS by claiming depth[v] < 0 with next_depth.
+ * out_frontier is zeroed by the pass. dist is fp64 (+inf unreached), depth
+ * int64 (-1 = UNREACHED). lw_sssp / lw_bfs run the whole traversal (one host
+ * synchronization per pass for the frontier size) and report the pass count.
+ * Workspace: lw_frontier_workspace(rows) bytes of device memory. */
+size_t lw_frontier_workspace(int64_t n_vertices);
+int lw_frontier_compact(const uint8_t* mask, int64_t n, int32_t* active, int64_t* count_dev,
+                        void* workspace, size_t workspace_bytes, uintptr_t stream);
+int lw_sssp_pass(const lw_csr_t* G, const int32_t* active, int64_t n_active, double* dist,
+                 uint8_t* out_frontier, int schedule, int64_t lanes, int64_t group_size,
+                 int64_t tiles_per_block, void* workspace, size_t workspace_bytes,
+                 uintptr_t stream);
+int lw_bfs_pass(const lw_csr_t* G, const int32_t* active, int64_t n_active, int64_t* depth,
+                int64_t next_depth, uint8_t* out_frontier, int schedule, int64_t lanes,
+                int64_t group_size, int64_t tiles_per_block, void* workspace,
+                size_t workspace_bytes, uintptr_t stream);
+int lw_sssp(const lw_csr_t* G, int64_t source, double* dist, int schedule, int64_t lanes,
+            int64_t group_size, int64_t tiles_per_block, void* workspace, size_t workspace_bytes,
+            int64_t* passes_out, uintptr_t stream);
+int lw_bfs(const lw_csr_t* G, int64_t source, int64_t* depth, int schedule, int64_t lanes,
+           int64_t group_size, int64_t tiles_per_block, void* workspace, size_t workspace_bytes,
+           int64_t* passes_out, uintptr_t stream);
+
 /* ---- ingestion (host-native; the input side of the path) ---------------------
  * Matrix Market coordinate text -> COO -> CSR. Replaces mmio.parse_matrix_market
  * (mmio.py:24-107) and sparse.coo_to_csr (sparse.py:130-150). Buffers are HOST

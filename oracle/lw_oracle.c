@@ -238,6 +238,69 @@ EXPORT void lwo_spmm_group_mapped(const int64_t* off, const int64_t* col, const 
     }
 }
 
+/* ---- SSSP / BFS (kernels.py:320-357 driving _fast.py:147-170) -------------------
+ * Frontier passes: active = flatnonzero(in_frontier) in vertex order, every
+ * out-edge relaxed serially, until the frontier is empty. Return the pass count. */
+EXPORT int64_t lwo_sssp(const int64_t* off, const int64_t* col, const double* w, int64_t n,
+                        int64_t src, double* dist) {
+    unsigned char* in = (unsigned char*)calloc((size_t)(n > 0 ? n : 1), 1);
+    unsigned char* out = (unsigned char*)calloc((size_t)(n > 0 ? n : 1), 1);
+    if (!in || !out) { free(in); free(out); return -1; }
+    for (int64_t i = 0; i < n; ++i) dist[i] = __builtin_inf();
+    dist[src] = 0.0;
+    in[src] = 1;
+    int64_t passes = 0;
+    for (;;) {
+        int any = 0;
+        memset(out, 0, (size_t)n);
+        for (int64_t u = 0; u < n; ++u) {
+            if (!in[u]) continue;
+            any = 1;
+            const double du = dist[u];
+            for (int64_t e = off[u]; e < off[u + 1]; ++e) {
+                const int64_t v = col[e];
+                const double nd = du + w[e];
+                if (nd < dist[v]) { dist[v] = nd; out[v] = 1; }
+            }
+        }
+        if (!any) break;
+        ++passes;
+        unsigned char* t = in; in = out; out = t;
+    }
+    free(in);
+    free(out);
+    return passes;
+}
+
+EXPORT int64_t lwo_bfs(const int64_t* off, const int64_t* col, int64_t n, int64_t src,
+                       int64_t* depth) {
+    unsigned char* in = (unsigned char*)calloc((size_t)(n > 0 ? n : 1), 1);
+    unsigned char* out = (unsigned char*)calloc((size_t)(n > 0 ? n : 1), 1);
+    if (!in || !out) { free(in); free(out); return -1; }
+    for (int64_t i = 0; i < n; ++i) depth[i] = -1;
+    depth[src] = 0;
+    in[src] = 1;
+    int64_t level = 0;
+    for (;;) {
+        int any = 0;
+        memset(out, 0, (size_t)n);
+        for (int64_t u = 0; u < n; ++u) {
+            if (!in[u]) continue;
+            any = 1;
+            for (int64_t e = off[u]; e < off[u + 1]; ++e) {
+                const int64_t v = col[e];
+                if (depth[v] < 0) { depth[v] = level + 1; out[v] = 1; }
+            }
+        }
+        if (!any) break;
+        ++level;
+        unsigned char* t = in; in = out; out = t;
+    }
+    free(in);
+    free(out);
+    return level;
+}
+
 /* ---- assignment maps (executor.py:132-209, 224-251) ------------------------
  * For every atom: the lane that processes it and the tile it is attributed to;
  * per lane: how many atoms it processes. Arrays may be NULL. lane_atoms is

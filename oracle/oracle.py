@@ -62,6 +62,8 @@ def lib():
             "lwo_spmm_merge_path": (_int, [_p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _int]),
             "lwo_spmm_group_mapped": (None, [_p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64,
                                              _int]),
+            "lwo_sssp": (_i64, [_p, _p, _p, _i64, _i64, _p]),
+            "lwo_bfs": (_i64, [_p, _p, _i64, _i64, _p]),
             "lwo_assign_thread_mapped": (None, [_p, _i64, _i64, _p, _p, _p]),
             "lwo_assign_merge_path": (None, [_p, _i64, _i64, _i64, _p, _p, _p]),
             "lwo_assign_group_mapped": (None, [_p, _i64, _i64, _i64, _i64, _p, _p, _p]),
@@ -207,6 +209,25 @@ def abs_spmm_sums(off, col, val, B) -> np.ndarray:
     prod = np.abs(_f64a(val)[:, None] * _f64a(B)[col])
     csum = np.concatenate([np.zeros((1, prod.shape[1])), np.cumsum(prod, axis=0)])
     return csum[off[1:]] - csum[off[:-1]]
+
+
+def sssp(off, col, w, source: int) -> np.ndarray:
+    """Frontier-pass SSSP exactly as the reference's numba path runs it."""
+    off, col, w = _i64a(off), _i64a(col), _f64a(w)
+    n = off.size - 1
+    dist = np.empty(n, dtype=np.float64)
+    if lib().lwo_sssp(_ptr(off), _ptr(col), _ptr(w), n, source, _ptr(dist)) < 0:
+        raise MemoryError("oracle sssp allocation failed")
+    return dist
+
+
+def bfs(off, col, source: int) -> np.ndarray:
+    off, col = _i64a(off), _i64a(col)
+    n = off.size - 1
+    depth = np.empty(n, dtype=np.int64)
+    if lib().lwo_bfs(_ptr(off), _ptr(col), n, source, _ptr(depth)) < 0:
+        raise MemoryError("oracle bfs allocation failed")
+    return depth
 
 
 def abs_row_sums(off, col, val, x) -> np.ndarray:

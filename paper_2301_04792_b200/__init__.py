@@ -13,11 +13,12 @@ from ._backend import (ENV_VAR, backend_name, cuda_active, cuda_available, numba
 from ._lib import BackendUnavailable
 from .device import (DeviceCsr, device_group_plan_prefix, device_merge_path_partition,
                      generate_banded_device, generate_rmat_csr)
-from .executor import (SENTINEL_TILE, CarryOut, CarryPolicy, ExecutorConfig, ImbalanceReport,
+from .executor import (SENTINEL_TILE, AtomicMinArray, atomic_min_real, CarryOut, CarryPolicy, ExecutorConfig, ImbalanceReport,
                        SUM_CARRIES, device_config, execute_merge_path, execute_tile_major,
                        fixup_combine, imbalance)
 from .kernels import (HeuristicConfig, choose_spmv_schedule, spmm, spmv, spmv_auto,
                       spmv_probe)
+from .traversal import UNREACHED, SsspState, bfs, bfs_pass, device_graph, sssp, sssp_init, sssp_pass
 from .schedules import (GroupMappedSchedule, GroupPlan, MergePathCoord, MergePathSchedule,
                         MergePathSlice, Schedule, ScheduleKind, ThreadMappedSchedule,
                         exclusive_prefix_sum, get_tile, group_plan, make_schedule,
@@ -34,6 +35,8 @@ from .work import (TileSet, csr_tile_set, infinite_range, lane_stride_range, ste
 __version__ = "0.1.0"
 
 __all__ = [
+    "AtomicMinArray", "SsspState", "UNREACHED", "atomic_min_real", "bfs", "bfs_pass",
+    "device_graph", "sssp", "sssp_init", "sssp_pass",
     "BackendUnavailable", "CarryOut", "CarryPolicy", "CooMatrix", "CsrMatrix", "Graph",
     "MatrixMarketError", "coo_to_csr", "csr_to_coo", "load_matrix_market", "parse_matrix_market",
     "transpose_csr", "validate_coo", "write_matrix_market", "DeviceCsr", "ENV_VAR",

@@ -29,6 +29,7 @@ SOURCES = [
     "spmv_work_oriented.cu",
     "spmv_group_mapped.cu",
     "spmm.cu",
+    "frontier.cu",
     "generators.cu",
     "mmio.cpp",
 ]

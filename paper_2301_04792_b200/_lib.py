@@ -50,6 +50,12 @@ EXPORTS = (
     "lw_spmm_work_oriented",
     "lw_spmm_group_mapped",
     "lw_spmm",
+    "lw_frontier_workspace",
+    "lw_frontier_compact",
+    "lw_sssp_pass",
+    "lw_bfs_pass",
+    "lw_sssp",
+    "lw_bfs",
     "lw_mm_parse_header",
     "lw_mm_parse_entries",
     "lw_coo_to_csr_host",
@@ -132,6 +138,16 @@ _SIGNATURES = {
     "lw_spmm_group_mapped": (ctypes.c_int, [_csr_p, _vp, _vp, _i64, _i64, _i64, _i64, _up]),
     "lw_spmm": (ctypes.c_int, [ctypes.c_int, _csr_p, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _sz,
                                _up]),
+    "lw_frontier_workspace": (_sz, [_i64]),
+    "lw_frontier_compact": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _sz, _up]),
+    "lw_sssp_pass": (ctypes.c_int, [_csr_p, _vp, _i64, _vp, _vp, ctypes.c_int, _i64, _i64, _i64,
+                                    _vp, _sz, _up]),
+    "lw_bfs_pass": (ctypes.c_int, [_csr_p, _vp, _i64, _vp, _i64, _vp, ctypes.c_int, _i64, _i64,
+                                   _i64, _vp, _sz, _up]),
+    "lw_sssp": (ctypes.c_int, [_csr_p, _i64, _vp, ctypes.c_int, _i64, _i64, _i64, _vp, _sz,
+                               ctypes.POINTER(_i64), _up]),
+    "lw_bfs": (ctypes.c_int, [_csr_p, _i64, _vp, ctypes.c_int, _i64, _i64, _i64, _vp, _sz,
+                              ctypes.POINTER(_i64), _up]),
     "lw_mm_parse_header": (ctypes.c_int, [ctypes.c_char_p, _sz, ctypes.POINTER(LwMmHeader),
                                           ctypes.c_char_p, _sz]),
     "lw_mm_parse_entries": (ctypes.c_int, [ctypes.c_char_p, _sz, ctypes.POINTER(LwMmHeader), _vp,

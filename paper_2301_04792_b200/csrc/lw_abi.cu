@@ -20,6 +20,12 @@ int hash_values(const int64_t*, int64_t, uint64_t, int, void*, cudaStream_t);
 int spmm(int, const lw_csr_t*, const void*, void*, int64_t, int64_t, int64_t, int64_t, void*, size_t, cudaStream_t);
 int64_t spmm_auto_lanes(int schedule, int64_t rows, int64_t nnz, int64_t n, int64_t gs, int64_t tpb);
 size_t spmm_wo_workspace(int64_t lanes, int64_t n);
+size_t frontier_workspace(int64_t n);
+int frontier_compact(const uint8_t*, int64_t, int32_t*, int64_t*, void*, cudaStream_t);
+int sssp_pass(const lw_csr_t*, const int32_t*, int64_t, double*, uint8_t*, int, int64_t, int64_t, int64_t, void*, cudaStream_t);
+int bfs_pass(const lw_csr_t*, const int32_t*, int64_t, int64_t*, int64_t, uint8_t*, int, int64_t, int64_t, int64_t, void*, cudaStream_t);
+int sssp_run(const lw_csr_t*, int64_t, double*, int, int64_t, int64_t, int64_t, void*, int64_t*, cudaStream_t);
+int bfs_run(const lw_csr_t*, int64_t, int64_t*, int, int64_t, int64_t, int64_t, void*, int64_t*, cudaStream_t);
 
 static int g_sm[64];
 static std::mutex g_sm_mu;
@@ -289,6 +295,72 @@ int lw_spmm_group_mapped(const lw_csr_t* A, const void* B, void* C, int64_t n, i
 int lw_spmm(int schedule, const lw_csr_t* A, const void* B, void* C, int64_t n, int64_t lanes,
             int64_t gs, int64_t tpb, void* ws, size_t ws_bytes, uintptr_t stream) {
     return spmm_entry(schedule, A, B, C, n, lanes, gs, tpb, ws, ws_bytes, stream);
+}
+
+/* ---- SSSP / BFS ------------------------------------------------------------------------ */
+
+size_t lw_frontier_workspace(int64_t n_vertices) {
+    return n_vertices < 0 ? 0 : frontier_workspace(n_vertices);
+}
+
+static int check_graph(const lw_csr_t* G, int schedule, int64_t lanes, int64_t gs, int64_t tpb,
+                       void* ws, size_t ws_bytes) {
+    int rc = check_csr(G);
+    if (rc) return rc;
+    if (G->rows != G->cols || lanes < 0) return LW_E_INVALID_ARG;
+    if (schedule != LW_THREAD_MAPPED && schedule != LW_MERGE_PATH && schedule != LW_GROUP_MAPPED)
+        return LW_E_INVALID_ARG;
+    if (schedule == LW_GROUP_MAPPED && (gs < 1 || tpb < 1)) return LW_E_INVALID_ARG;
+    if (G->rows > 0x7fffffffLL) return LW_E_UNSUPPORTED;   // active lists are int32
+    if (!ws || ws_bytes < frontier_workspace(G->rows)) return LW_E_WORKSPACE;
+    return LW_OK;
+}
+
+int lw_frontier_compact(const uint8_t* mask, int64_t n, int32_t* active, int64_t* count_dev,
+                        void* ws, size_t ws_bytes, uintptr_t stream) {
+    if (n < 0 || (n > 0 && (!mask || !active)) || !count_dev) return LW_E_INVALID_ARG;
+    if (!ws || ws_bytes < frontier_workspace(n)) return LW_E_WORKSPACE;
+    return frontier_compact(mask, n, active, count_dev, ws, (cudaStream_t)stream);
+}
+
+int lw_sssp_pass(const lw_csr_t* G, const int32_t* active, int64_t n_active, double* dist,
+                 uint8_t* out_frontier, int schedule, int64_t lanes, int64_t gs, int64_t tpb,
+                 void* ws, size_t ws_bytes, uintptr_t stream) {
+    int rc = check_graph(G, schedule, lanes, gs, tpb, ws, ws_bytes);
+    if (rc) return rc;
+    if (n_active < 0 || n_active > G->rows || (n_active > 0 && !active)) return LW_E_INVALID_ARG;
+    if (G->rows > 0 && (!dist || !out_frontier)) return LW_E_INVALID_ARG;
+    return sssp_pass(G, active, n_active, dist, out_frontier, schedule, lanes, gs, tpb, ws,
+                     (cudaStream_t)stream);
+}
+
+int lw_bfs_pass(const lw_csr_t* G, const int32_t* active, int64_t n_active, int64_t* depth,
+                int64_t next_depth, uint8_t* out_frontier, int schedule, int64_t lanes, int64_t gs,
+                int64_t tpb, void* ws, size_t ws_bytes, uintptr_t stream) {
+    int rc = check_graph(G, schedule, lanes, gs, tpb, ws, ws_bytes);
+    if (rc) return rc;
+    if (n_active < 0 || n_active > G->rows || (n_active > 0 && !active)) return LW_E_INVALID_ARG;
+    if (G->rows > 0 && (!depth || !out_frontier)) return LW_E_INVALID_ARG;
+    return bfs_pass(G, active, n_active, depth, next_depth, out_frontier, schedule, lanes, gs, tpb,
+                    ws, (cudaStream_t)stream);
+}
+
+int lw_sssp(const lw_csr_t* G, int64_t source, double* dist, int schedule, int64_t lanes,
+            int64_t gs, int64_t tpb, void* ws, size_t ws_bytes, int64_t* passes_out,
+            uintptr_t stream) {
+    int rc = check_graph(G, schedule, lanes, gs, tpb, ws, ws_bytes);
+    if (rc) return rc;
+    if (source < 0 || source >= G->rows || !dist) return LW_E_INVALID_ARG;
+    return sssp_run(G, source, dist, schedule, lanes, gs, tpb, ws, passes_out, (cudaStream_t)stream);
+}
+
+int lw_bfs(const lw_csr_t* G, int64_t source, int64_t* depth, int schedule, int64_t lanes,
+           int64_t gs, int64_t tpb, void* ws, size_t ws_bytes, int64_t* passes_out,
+           uintptr_t stream) {
+    int rc = check_graph(G, schedule, lanes, gs, tpb, ws, ws_bytes);
+    if (rc) return rc;
+    if (source < 0 || source >= G->rows || !depth) return LW_E_INVALID_ARG;
+    return bfs_run(G, source, depth, schedule, lanes, gs, tpb, ws, passes_out, (cudaStream_t)stream);
 }
 
 int lw_rmat_keys(int32_t scale, int64_t edge_begin, int64_t n_edges, uint32_t t_a, uint32_t t_ab,

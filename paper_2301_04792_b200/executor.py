@@ -19,6 +19,7 @@ GPU) and are not on the SpMV path.
 from __future__ import annotations
 
 import operator
+import threading
 from dataclasses import dataclass, field, replace
 from typing import Callable, NamedTuple
 
@@ -28,7 +29,7 @@ from .schedules import (GroupMappedSchedule, MergePathSchedule, ScheduleKind,
                         ThreadMappedSchedule, merge_path_partition, num_blocks)
 from .work import tile_offsets
 
-__all__ = ["SENTINEL_TILE", "ExecutorConfig", "CarryOut", "CarryPolicy", "SUM_CARRIES",
+__all__ = ["AtomicMinArray", "atomic_min_real", "SENTINEL_TILE", "ExecutorConfig", "CarryOut", "CarryPolicy", "SUM_CARRIES",
            "ImbalanceReport", "imbalance", "execute_tile_major", "execute_merge_path",
            "fixup_combine", "device_config"]
 
@@ -228,3 +229,31 @@ def fixup_combine(carries, combine) -> None:
     for c in carries:
         if c.tile != SENTINEL_TILE:
             combine(c.tile, c.partial)
+
+
+class AtomicMinArray:
+    """Shared array of non-negative reals (or +inf) with atomic min (reference
+    executor.py:254-283). The device kernels do the same with atomicMin on the
+    fp64 bit pattern (csrc/frontier.cu), which orders like the values precisely
+    because they are non-negative; host code gets this lock-based twin."""
+
+    def __init__(self, values: np.ndarray):
+        self.values = np.asarray(values, dtype=np.float64)
+        if self.values.size and np.nanmin(self.values) < 0:
+            raise ValueError("slots must hold non-negative reals or +inf")
+        self._lock = threading.Lock()
+
+    def atomic_min(self, index: int, candidate: float) -> float:
+        """Set slot ``index`` to min(slot, candidate); returns the prior value."""
+        if not candidate >= 0:
+            raise ValueError("candidate must be non-negative")
+        with self._lock:
+            previous = float(self.values[index])
+            if candidate < previous:
+                self.values[index] = candidate
+            return previous
+
+
+def atomic_min_real(slots: AtomicMinArray, index: int, candidate: float) -> float:
+    """Function-call spelling of :meth:`AtomicMinArray.atomic_min`."""
+    return slots.atomic_min(index, candidate)

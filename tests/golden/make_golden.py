@@ -300,6 +300,42 @@ def make_mmio():
         col_idx=pack(cols_)[1], err_texts=np.array(MM_ERROR_TEXTS), err_msgs=np.array(msgs))
 
 
+def make_traversal():
+    """sssp / bfs (numba) and the serial references dijkstra / serial_bfs
+    (kernels.py:320-357, reference.py) on graphs with unreachable parts,
+    self-loops, integer and real non-negative weights."""
+    from lanework import reference as ref
+
+    rng = np.random.default_rng(99)
+    offs, cols, ws, srcs, dists, dijk, depths, sbfs = [], [], [], [], [], [], [], []
+    for k in range(14):
+        n = int(rng.integers(2, 300))
+        if k % 3 == 0:
+            m = lw.generate_power_law_csr(n, 4.0, 1.3, seed=int(rng.integers(1 << 30)))
+        else:
+            m = lw.generate_random_csr(n, n, int(rng.integers(0, min(n * n, 6 * n) + 1)),
+                                       seed=int(rng.integers(1 << 30)))
+        if k % 2 == 0:
+            m.values = rng.integers(0, 10, size=m.nnz).astype(np.float64)
+        else:
+            m.values = np.abs(m.values)
+        g = lw.Graph(m)
+        src = int(rng.integers(0, n))
+        offs.append(m.row_offsets)
+        cols.append(m.col_indices)
+        ws.append(m.values)
+        srcs.append(src)
+        dists.append(lw.sssp(g, src))
+        dijk.append(ref.dijkstra(g, src))
+        depths.append(lw.bfs(g, src))
+        sbfs.append(ref.serial_bfs(g, src))
+    np.savez_compressed(
+        OUT / "traversal.npz", off=pack(offs)[0], off_idx=pack(offs)[1], col=pack(cols)[0],
+        w=pack(ws)[0], col_idx=pack(cols)[1], src=np.array(srcs),
+        dist=pack(dists)[0], dijkstra=pack(dijk)[0], depth=pack(depths)[0],
+        serial_bfs=pack(sbfs)[0], v_idx=pack(dists)[1])
+
+
 def make_generators():
     out = {}
     cases = [("random", (40, 30, 200, 1)), ("random", (300, 200, 5000, 7)),
@@ -319,8 +355,9 @@ def make_generators():
 
 if __name__ == "__main__":
     print("reference:", lw.__file__, "backend:", lw.backend_name())
-    which = set(sys.argv[1:]) or {"schedules", "spmv", "spmm", "mmio", "generators"}
-    for name in ("schedules", "spmv", "spmm", "mmio", "generators"):
+    names = ("schedules", "spmv", "spmm", "mmio", "traversal", "generators")
+    which = set(sys.argv[1:]) or set(names)
+    for name in names:
         if name in which:
             globals()[f"make_{name}"]()
     for f in sorted(OUT.glob("*.npz")):

@@ -310,3 +310,16 @@ def test_backend_seam_has_no_cpu_fallback(monkeypatch):
         m = lw.CsrMatrix(2, 2, [0, 2, 3], [0, 1, 1], [1.0, 2.0, 3.0])
         with pytest.raises(lw.BackendUnavailable):
             lw.spmv(m, np.ones(2))
+
+
+def test_atomic_min_array_semantics():
+    """executor.AtomicMinArray (reference executor.py:254-283)."""
+    import paper_2301_04792_b200 as lwb
+
+    a = lwb.AtomicMinArray(np.array([np.inf, 2.0]))
+    assert a.atomic_min(0, 3.0) == np.inf and a.values[0] == 3.0
+    assert lwb.atomic_min_real(a, 1, 5.0) == 2.0 and a.values[1] == 2.0
+    with pytest.raises(ValueError):
+        a.atomic_min(0, -1.0)
+    with pytest.raises(ValueError):
+        lwb.AtomicMinArray(np.array([-1.0]))

@@ -129,3 +129,17 @@ def test_spmm_column_slices_equal_spmv():
         C = oracle.spmm(off, col, val, B, kind, lanes=7)
         for c in range(6):
             np.testing.assert_array_equal(C[:, c], oracle.spmv(off, col, val, B[:, c], kind, lanes=7))
+
+
+def test_traversal_oracle_matches_reference(golden):
+    """Oracle frontier SSSP/BFS == lanework.sssp / bfs == dijkstra / serial_bfs, bit for bit."""
+    g = golden["traversal"]
+    for k, src in enumerate(g["src"]):
+        off, col = unpack(g["off"], g["off_idx"], k), unpack(g["col"], g["col_idx"], k)
+        w = unpack(g["w"], g["col_idx"], k)
+        dist = oracle.sssp(off, col, w, int(src))
+        np.testing.assert_array_equal(dist, unpack(g["dist"], g["v_idx"], k))
+        np.testing.assert_array_equal(dist, unpack(g["dijkstra"], g["v_idx"], k))
+        depth = oracle.bfs(off, col, int(src))
+        np.testing.assert_array_equal(depth, unpack(g["depth"], g["v_idx"], k))
+        np.testing.assert_array_equal(depth, unpack(g["serial_bfs"], g["v_idx"], k))
