@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(WoCfg<ValT>::NT)
                 run_row = t1; run_val = tv; run_has = tail;
             }
         }
-        __syncthreads();   // s_end / s_seg / s_flag are rewritten by the next chunk
+        if (jc + 1 < J) __syncthreads();   // s_end / s_seg / s_flag are rewritten by the next chunk
     }
     if (tid == 0) {
         const bool live = run_has && run_row >= 0 && run_row < A.rows;
