@@ -8,8 +8,8 @@
 //
 // Device mapping: a lane is a TEAM of TS threads (TS = power of two <= 32) that
 // covers a slab of TS*VEC consecutive columns, VEC columns per thread with one
-// 16-byte load of B / store of C (VEC = 1 when n or the pointers do not allow
-// it). Slabs wider than 32*VEC are walked one after the other, re-reading the
+// 16-byte load of B / store of C (VEC = 4 fp32, 2 fp64; 1 when n or the pointers
+// do not allow it). Slabs wider than 32*VEC are walked one after the other, re-reading the
 // lane's atoms (the reference's column loop). A team reads each atom's column
 // index and value once (the same address for the whole team, one L1 request)
 // and gathers a contiguous TS*VEC-wide row segment of B. Sums are fp64 and follow
@@ -18,13 +18,14 @@
 
 namespace lw {
 
-int mp_bound_tiles(const lw_csr_t* A, int64_t lanes, int64_t* tiles, cudaStream_t s);
+int mp_bound_tiles(const lw_csr_t* A, int64_t lanes, int64_t J, int64_t S, int64_t* tiles,
+                   cudaStream_t s);
 int64_t group_auto_lanes(int64_t rows, int64_t gs, int64_t tpb);
 
 constexpr int MM_NT = 256;   // threads per CTA (a multiple of every team size)
-constexpr int MM_U = 4;      // atoms per batch: col/val/B loads in flight per thread
+constexpr int MM_U = 8;      // atoms per batch: col/val/B loads in flight per thread
 
-// VEC consecutive values of B / C
+// VEC consecutive values of B / C (16-byte vectors: float4 / double2)
 template <class ValT, int VEC>
 __device__ __forceinline__ void ld_row(const ValT* p, ValT* v) {
     if constexpr (VEC == 4) {
@@ -47,6 +48,12 @@ __device__ __forceinline__ void st_row(ValT* p, const double* a) {
         p[0] = (ValT)a[0];
     }
 }
+
+// atoms per batch of the atom-major walk: about 16 B-row values per thread in flight
+template <int VEC>
+struct MmU {
+    static constexpr int U = VEC >= 4 ? 4 : 8;
+};
 
 // Accumulate atoms [a, a+cnt) (cnt <= MM_U, all in the same row) into acc.
 template <class OffT, class ValT, int VEC>
@@ -113,12 +120,16 @@ __global__ void __launch_bounds__(MM_NT)
 // Lane k walks diagonals [min(k*items,total), min((k+1)*items,total)): rows
 // [t0, t1) end inside its slice and are assigned; the partial row t1 becomes the
 // lane's carry (n values), added in lane order by k_spmm_carry_fixup.
+#ifndef LW_MM_WO_MINB
+#define LW_MM_WO_MINB 4
+#endif
 template <class OffT, class ValT, int VEC>
-__global__ void __launch_bounds__(MM_NT)
+__global__ void __launch_bounds__(MM_NT, LW_MM_WO_MINB)
     k_spmm_work_oriented(Csr<OffT, ValT> A, const ValT* __restrict__ B, ValT* __restrict__ C,
                          int64_t n, int64_t lanes, int64_t items, int lg_ts,
                          const int64_t* __restrict__ bound_tile, int64_t* __restrict__ carry_tile,
                          double* __restrict__ carry_val) {
+    constexpr int U = MmU<VEC>::U;
     const int64_t gt = (int64_t)blockIdx.x * MM_NT + threadIdx.x;
     const int64_t lane = gt >> lg_ts;
     const int tl = (int)(gt & ((1 << lg_ts) - 1));
@@ -135,24 +146,53 @@ __global__ void __launch_bounds__(MM_NT)
     for (int64_t cs = 0; cs < n; cs += sw) {
         const int64_t c = cs + (int64_t)tl * VEC;
         const bool active = c < n;
-        int64_t a = a0;
-        for (int64_t t = t0; t < t1; ++t) {
-            const int64_t e = (int64_t)__ldg(A.off + t + 1);
-            double acc[VEC];
+        // atom-major walk: batches of U atoms cross row ends, so every batch
+        // keeps U gathers of B in flight however short the rows are; the next
+        // row end is loaded one row ahead
+        int64_t t = t0;
+        int64_t re = t < t1 ? (int64_t)__ldg(A.off + t + 1) : a1;
+        int64_t re2 = t + 1 < t1 ? (int64_t)__ldg(A.off + t + 2) : a1;
+        double acc[VEC];
 #pragma unroll
-            for (int j = 0; j < VEC; ++j) acc[j] = 0.0;
-            mm_range<OffT, ValT, VEC>(A, B, n, c, active, a, e, acc);
+        for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
+        auto finish_row = [&]() {
             if (active) st_row<ValT, VEC>(C + t * n + c, acc);
-            a = e;
-        }
-        if (carry && active) {
-            double acc[VEC];
 #pragma unroll
-            for (int j = 0; j < VEC; ++j) acc[j] = 0.0;
-            mm_range<OffT, ValT, VEC>(A, B, n, c, active, ts, a1, acc);
+            for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
+            ++t;
+            re = re2;
+            re2 = t + 1 < t1 ? (int64_t)__ldg(A.off + t + 2) : a1;
+        };
+        for (int64_t a = a0; a < a1; a += U) {
+            const int cnt = (int)min((int64_t)U, a1 - a);
+            int32_t col[U];
+            ValT val[U];
+            ValT b[U][VEC];
 #pragma unroll
-            for (int j = 0; j < VEC; ++j) carry_val[lane * n + c + j] = acc[j];
+            for (int k = 0; k < U; ++k) {
+                col[k] = k < cnt ? __ldg(A.col + a + k) : 0;
+                val[k] = k < cnt ? __ldg(A.val + a + k) : (ValT)0;
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                if (active && k < cnt) ld_row<ValT, VEC>(B + (int64_t)col[k] * n + c, b[k]);
+                else
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) b[k][v] = (ValT)0;
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                if (k < cnt) {
+                    while (t < t1 && re <= a + k) finish_row();
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) acc[v] = fma((double)val[k], (double)b[k][v], acc[v]);
+                }
+            }
         }
+        while (t < t1) finish_row();   // rows ending at a1, and empty rows
+        if (carry && active)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) carry_val[lane * n + c + v] = acc[v];
     }
 }
 
@@ -299,7 +339,7 @@ static int spmm_typed(int schedule, const lw_csr_t* H, const void* Bp, void* Cp,
             double* c_val = (double*)(w + up((size_t)(lanes + 1) * 8) + up((size_t)lanes * 8));
             const int64_t total = A.rows + A.nnz;
             const int64_t items = total > 0 ? ceil_div(total, lanes) : 0;
-            int rc = mp_bound_tiles(H, lanes, tiles, s);
+            int rc = mp_bound_tiles(H, lanes, 1, items, tiles, s);
             if (rc) return rc;
             LW_MM_DISPATCH(k_spmm_work_oriented, A, B, C, n, lanes, items, sh.lg_ts, tiles, c_tile,
                            c_val);

@@ -601,16 +601,19 @@ static int launch_search(const OffT* off, int64_t rows, int64_t nnz, int64_t n_b
     return LW_OK;
 }
 
-// Tile of every lane boundary of merge_path_partition(ts, lanes) (coords[:, 0]),
-// for the SpMM work_oriented kernel. tiles: device int64[lanes+1].
-int mp_bound_tiles(const lw_csr_t* A, int64_t lanes, int64_t* tiles, cudaStream_t s) {
+// Tiles of the chunk boundaries of merge_path_partition(ts, lanes) with each lane
+// cut into J chunks of at most S items (boundary b = lane*J + chunk, as for the
+// SpMV chunk kernel; J = 1 gives the partition's coords[:, 0]), for the SpMM
+// work_oriented kernel. tiles: device int64[lanes*J + 1].
+int mp_bound_tiles(const lw_csr_t* A, int64_t lanes, int64_t J, int64_t S, int64_t* tiles,
+                   cudaStream_t s) {
     const int64_t total = A->rows + A->nnz;
     const int64_t items = total > 0 ? ceil_div(total, lanes) : 0;
     if (A->offset_bits == 32)
-        return launch_search<int32_t>((const int32_t*)A->row_offsets, A->rows, A->nnz, lanes + 1, 1,
-                                      items, items, tiles, nullptr, s);
-    return launch_search<int64_t>((const int64_t*)A->row_offsets, A->rows, A->nnz, lanes + 1, 1,
-                                  items, items, tiles, nullptr, s);
+        return launch_search<int32_t>((const int32_t*)A->row_offsets, A->rows, A->nnz, lanes * J + 1,
+                                      J, items, S, tiles, nullptr, s);
+    return launch_search<int64_t>((const int64_t*)A->row_offsets, A->rows, A->nnz, lanes * J + 1, J,
+                                  items, S, tiles, nullptr, s);
 }
 
 int merge_path_partition(int64_t rows, int64_t nnz, const void* off, int bits, int64_t lanes,
