@@ -16,9 +16,11 @@
  *     memory behind the caller's back (workspace sizes come from *_workspace()).
  *   - Return value: 0 on success, otherwise a cudaError_t value (< 10000) or an
  *     LW_E_* code (>= 10000). lw_error_string() maps either to text.
- *   - Arithmetic: products and sums are carried in fp64 for both fp32 and fp64
- *     inputs; y is rounded to the input dtype once per row (plus once per carry
- *     fix-up for rows a work_oriented partition cuts).
+ *   - Arithmetic: thread_mapped / group_mapped SpMV and every SpMM sum in fp64
+ *     for fp32 and fp64 inputs; the work_oriented SpMV chunk scan adds at most
+ *     IPT + 5 + NT/32 products in the value precision and carries partials across
+ *     chunks and lanes in fp64. y is rounded to the input dtype once per row (plus
+ *     once per carry fix-up for rows a work_oriented partition cuts).
  */
 #ifndef LW_B200_H
 #define LW_B200_H
