@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--mode", default="spmv", choices=["spmv", "power"],
                     help="spmv: one y=Ax per step (C3 headline); power: C5 power iteration")
     ap.add_argument("--iters", type=int, default=20, help="power iterations per step (C5)")
+    ap.add_argument("--chunks", type=int, default=0,
+                    help="power mode: row chunks per shard whose all-gathers overlap the next "
+                         "chunk's SpMV (0 = 4 when N > 1, else 1)")
     ap.add_argument("--items", type=int, default=0,
                     help="work_oriented items per lane (0 = library default)")
     return ap.parse_args()
@@ -244,19 +247,26 @@ def power_arm(args):
     torch.cuda.empty_cache()
     cfg = lwb.ExecutorConfig(schedule=lwb.ScheduleKind.MERGE_PATH)
     y_local = torch.empty(A.rows, dtype=A.dtype, device=dev)
+    chunks = args.chunks or (4 if world > 1 else 1)
+    pieces = {}   # (r0, r1) -> (row-slice view, output view), built once
     spmv_ev = []
 
-    def local_spmv(x):
+    def local_spmv(x, r0=0, r1=None):
+        r1 = A.rows if r1 is None else r1
+        if (r0, r1) not in pieces:
+            pieces[(r0, r1)] = (A if (r0, r1) == (0, A.rows) else A.row_slice(r0, r1),
+                                y_local[r0:r1])
+        Ak, yk = pieces[(r0, r1)]
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        lwb.spmv(A, x, cfg, out=y_local)
+        lwb.spmv(Ak, x, cfg, out=yk)
         e1.record()
         spmv_ev.append((e0, e1))
-        return y_local
+        return yk
 
     for _ in range(max(args.warmup, 3)):
-        power_iteration(local_spmv, n, shard, 2, dtype=A.dtype, device=dev)
+        power_iteration(local_spmv, n, shard, 2, dtype=A.dtype, device=dev, chunks=chunks)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -266,7 +276,8 @@ def power_arm(args):
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record()
         for _ in range(args.steps):
-            x, norms = power_iteration(local_spmv, n, shard, args.iters, dtype=A.dtype, device=dev)
+            x, norms = power_iteration(local_spmv, n, shard, args.iters, dtype=A.dtype, device=dev,
+                                       chunks=chunks)
         t1.record()
         torch.cuda.synchronize()
     if world > 1:
@@ -285,11 +296,12 @@ def power_arm(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f32" if args.dtype == "fp32" else "f64",
         "data": "synthetic",
         "config": {"workload": f"rmat{args.scale}-ef{args.edge_factor}-seed{args.seed}-power{args.iters}",
-                   "rows": n, "nnz": nnz_total, "parallelism": f"rows{world}" if world > 1 else "single"},
+                   "rows": n, "nnz": nnz_total, "parallelism": f"rows{world}" if world > 1 else "single",
+                   "overlap_chunks": chunks},
         "breakdown_ms": {"spmv_max_rank": round(spmv_ms, 3),
                          "allgather_normalise": round(ms - spmv_ms, 3)},
         "final_norm": norms[-1] if norms else None,
-        "gpu_launches": 3 * args.iters * args.steps,
+        "gpu_launches": 3 * chunks * args.iters * args.steps,
         "clocks": clocks.summary(),
     }
     if rank == 0:

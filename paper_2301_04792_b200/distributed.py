@@ -14,7 +14,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["nnz_balanced_bounds", "shard_of", "power_iteration", "RowShard"]
+__all__ = ["nnz_balanced_bounds", "shard_of", "power_iteration", "chunk_bounds", "RowShard"]
 
 
 def nnz_balanced_bounds(row_offsets, parts: int) -> np.ndarray:
@@ -63,15 +63,31 @@ def shard_of(host_csr, bounds, rank: int):
                      host_csr.values[a0:a1])
 
 
+def chunk_bounds(rows: int, chunks: int) -> np.ndarray:
+    """Split local rows [0, rows) into ``chunks`` contiguous, near-equal pieces."""
+    chunks = max(1, int(chunks))
+    return (np.arange(chunks + 1, dtype=np.int64) * rows) // chunks
+
+
 def power_iteration(local_spmv, n: int, shard: RowShard, iters: int, group=None, x0=None,
-                    device=None, dtype=None, on_iter=None):
+                    device=None, dtype=None, on_iter=None, chunks: int = 1):
     """x_{k+1} = A x_k / ||A x_k||_2 for ``iters`` iterations, y all-gathered.
 
-    ``local_spmv(x_full) -> y_shard`` computes this rank's rows. The uneven
-    shards are padded to the largest shard so a single all_gather_into_tensor
-    (NCCL all-gather over NVLink) moves them; every rank then holds the full y,
-    normalises it locally (identical arithmetic on every rank, no all-reduce)
-    and uses it as the next x. Returns (x, norms) with norms[k] = ||A x_k||.
+    ``local_spmv(x_full) -> y_shard`` computes this rank's rows; with
+    ``chunks > 1`` it is called as ``local_spmv(x_full, r0, r1)`` for local row
+    ranges and must return those rows.
+
+    chunks == 1: the uneven shards are padded to the largest shard so one
+    all_gather_into_tensor (NCCL over NVLink) moves them.
+    chunks > 1: the shard is cut into row chunks (every rank uses the same count,
+    so chunk k of every rank is exchanged together); chunk k's all-gather is
+    issued asynchronously as soon as its SpMV is enqueued, so it runs on NCCL's
+    stream while chunk k+1's SpMV computes (at 8 GPUs the exchange
+    is as long as the SpMV, so it has to overlap). One index_select then puts the
+    rank-major, chunk-major pieces back in row order.
+
+    Every rank normalises the same full y locally (identical arithmetic on every
+    rank, no all-reduce). Returns (x, norms) with norms[k] = ||A x_k||.
     """
     import torch
     import torch.distributed as dist
@@ -83,20 +99,47 @@ def power_iteration(local_spmv, n: int, shard: RowShard, iters: int, group=None,
         x = torch.full((n,), 1.0 / np.sqrt(n), dtype=dtype or torch.float32, device=device)
     else:
         x = x0
+    chunks = max(1, int(chunks))
     even = all(c == width for c in counts)
-    if world > 1:
+    if world > 1 and chunks == 1:
         gathered = torch.empty(world * width, dtype=x.dtype, device=x.device)
         send = torch.zeros(width, dtype=x.dtype, device=x.device)
+    if chunks > 1:
+        # per-rank chunk sizes (every rank derives all of them from the bounds)
+        cb = [chunk_bounds(c, chunks) for c in counts]
+        widths = [max(int(cb[r][k + 1] - cb[r][k]) for r in range(len(counts))) for k in range(chunks)]
+        mine = cb[shard.rank] if world > 1 else chunk_bounds(shard.rows, chunks)
+        if world > 1:
+            sends = [torch.zeros(w, dtype=x.dtype, device=x.device) for w in widths]
+            recvs = [torch.empty(world * w, dtype=x.dtype, device=x.device) for w in widths]
+            # row order: rank r, chunk k, element j  <-  recvs[k][r * widths[k] + j]
+            offs = np.concatenate([[0], np.cumsum([world * w for w in widths])])
+            idx = np.concatenate([offs[k] + r * widths[k] + np.arange(cb[r][k + 1] - cb[r][k])
+                                  for r in range(world) for k in range(chunks)]).astype(np.int64)
+            order = torch.as_tensor(idx, device=x.device)
     norms = []
     for k in range(iters):
-        y_local = local_spmv(x)
-        if world > 1:
-            send[: shard.rows].copy_(y_local)
-            dist.all_gather_into_tensor(gathered, send, group=group)
-            y = gathered if even else torch.cat(
-                [gathered[r * width: r * width + counts[r]] for r in range(world)])
+        if chunks == 1:
+            y_local = local_spmv(x)
+            if world > 1:
+                send[: shard.rows].copy_(y_local)
+                dist.all_gather_into_tensor(gathered, send, group=group)
+                y = gathered if even else torch.cat(
+                    [gathered[r * width: r * width + counts[r]] for r in range(world)])
+            else:
+                y = y_local
+        elif world > 1:
+            works = []
+            for c in range(chunks):
+                r0, r1 = int(mine[c]), int(mine[c + 1])
+                sends[c][: r1 - r0].copy_(local_spmv(x, r0, r1))
+                works.append(dist.all_gather_into_tensor(recvs[c], sends[c], group=group,
+                                                         async_op=True))
+            for w in works:
+                w.wait()
+            y = torch.cat(recvs).index_select(0, order)
         else:
-            y = y_local
+            y = torch.cat([local_spmv(x, int(mine[c]), int(mine[c + 1])) for c in range(chunks)])
         # ||y|| accumulated in fp64 on the device; no host sync inside the loop
         nrm = torch.linalg.vector_norm(y, dtype=torch.float64)
         norms.append(nrm)

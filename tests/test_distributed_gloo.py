@@ -53,7 +53,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, chunks=1):
     from oracle import oracle
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -64,24 +64,29 @@ def _worker(rank, world, port, out):
         shard = RowShard(b, rank)
         mine = shard_of(m, b, rank)
 
-        def local(x):
-            y = oracle.spmv(mine.row_offsets, mine.col_indices, mine.values,
+        def local(x, r0=0, r1=None):
+            part = shard_of(mine, [0, r0, mine.rows if r1 is None else r1], 1)
+            y = oracle.spmv(part.row_offsets, part.col_indices, part.values,
                             x.double().numpy(), "merge-path", lanes=32)
             return torch.from_numpy(y).to(x.dtype)
 
-        x, norms = power_iteration(local, m.rows, shard, iters=8, dtype=torch.float64)
+        x, norms = power_iteration(local, m.rows, shard, iters=8, dtype=torch.float64,
+                                   chunks=chunks)
         out[rank] = (x.numpy().copy(), list(norms))
     finally:
         dist.destroy_process_group()
 
 
-def test_power_iteration_world2_matches_single_process():
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_power_iteration_world2_matches_single_process(chunks):
+    """chunks=3: the overlapped path (per-chunk async all-gathers + reorder)."""
     from oracle import oracle
 
     port = _free_port()
     mgr = mp.get_context("spawn").Manager()
     out = mgr.dict()
-    mp.start_processes(_worker, args=(2, port, out), nprocs=2, join=True, start_method="spawn")
+    mp.start_processes(_worker, args=(2, port, out, chunks), nprocs=2, join=True,
+                       start_method="spawn")
     m = lw.generate_power_law_csr(4000, 10.0, 1.2, seed=7)
     x = np.full(m.rows, 1.0 / np.sqrt(m.rows))
     norms = []
@@ -95,3 +100,24 @@ def test_power_iteration_world2_matches_single_process():
         np.testing.assert_allclose(xr, x, rtol=1e-10, atol=1e-13)
         np.testing.assert_allclose(nr, norms, rtol=1e-12)
     np.testing.assert_array_equal(out[0][0], out[1][0])  # ranks stay identical
+
+
+def test_chunked_single_process_equals_plain():
+    """world 1: the chunked driver computes the same iterates as the plain one."""
+    from oracle import oracle
+
+    m = lw.generate_power_law_csr(2000, 8.0, 1.3, seed=11)
+    b = nnz_balanced_bounds(m.row_offsets, 1)
+    shard = RowShard(b, 0)
+
+    def local(x, r0=0, r1=None):
+        part = shard_of(m, [0, r0, m.rows if r1 is None else r1], 1)
+        y = oracle.spmv(part.row_offsets, part.col_indices, part.values, x.double().numpy(),
+                        "merge-path", lanes=16)
+        return torch.from_numpy(y)
+
+    x1, n1 = power_iteration(local, m.rows, shard, iters=5, dtype=torch.float64)
+    x4, n4 = power_iteration(local, m.rows, shard, iters=5, dtype=torch.float64, chunks=4)
+    # the per-chunk SpMV cuts rows differently (merge-path lanes), so only FP order differs
+    np.testing.assert_allclose(x4.numpy(), x1.numpy(), rtol=1e-12, atol=1e-15)
+    np.testing.assert_allclose(n4, n1, rtol=1e-12)
