@@ -143,6 +143,116 @@ static int scan_run(F f, int64_t n, int64_t* sums, int64_t* out, int32_t* compac
     return LW_OK;
 }
 
+// ---- fused frontier scan: active[] and frontier offsets fo[] in one sweep ---------------
+// Item v contributes (mask[v] != 0, degree(v) if in the frontier): the exclusive
+// prefix of the first gives v's slot in active[], of the second the offset of
+// its out-edges in the frontier tile set. sums2 holds per-block pairs.
+struct Pair {
+    int64_t a, b;
+};
+
+__device__ __forceinline__ Pair block_excl_scan2(Pair v, Pair* s_warp, Pair* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    Pair x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int64_t oa = __shfl_up_sync(0xffffffffu, x.a, d);
+        const int64_t ob = __shfl_up_sync(0xffffffffu, x.b, d);
+        if (lane >= d) { x.a += oa; x.b += ob; }
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        Pair w = lane < SC_NT / 32 ? s_warp[lane] : Pair{0, 0};
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int64_t oa = __shfl_up_sync(0xffffffffu, w.a, d);
+            const int64_t ob = __shfl_up_sync(0xffffffffu, w.b, d);
+            if (lane >= d) { w.a += oa; w.b += ob; }
+        }
+        if (lane < SC_NT / 32) s_warp[lane] = w;
+    }
+    __syncthreads();
+    const Pair before = warp ? s_warp[warp - 1] : Pair{0, 0};
+    if (total) *total = s_warp[SC_NT / 32 - 1];
+    return Pair{before.a + x.a - v.a, before.b + x.b - v.b};
+}
+
+template <class OffT>
+__device__ __forceinline__ Pair frontier_item(const uint8_t* mask, const OffT* off, int64_t v) {
+    if (!mask[v]) return Pair{0, 0};
+    return Pair{1, (int64_t)__ldg(off + v + 1) - (int64_t)__ldg(off + v)};
+}
+
+template <class OffT>
+__global__ void __launch_bounds__(SC_NT)
+    k_fscan_up(const uint8_t* __restrict__ mask, const OffT* __restrict__ off, int64_t n, Pair* sums) {
+    __shared__ Pair s_warp[SC_NT / 32];
+    const int64_t base = (int64_t)blockIdx.x * SC_TILE + (int64_t)threadIdx.x * SC_IPT;
+    Pair t{0, 0};
+#pragma unroll
+    for (int k = 0; k < SC_IPT; ++k)
+        if (base + k < n) {
+            const Pair it = frontier_item(mask, off, base + k);
+            t.a += it.a;
+            t.b += it.b;
+        }
+    Pair tot;
+    block_excl_scan2(t, s_warp, &tot);
+    if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(SC_NT) k_fscan_sums(Pair* sums, int64_t m) {
+    __shared__ Pair s_warp[SC_NT / 32];
+    Pair carry{0, 0};
+    for (int64_t c = 0; c < m; c += SC_NT) {
+        const int64_t i = c + threadIdx.x;
+        const Pair v = i < m ? sums[i] : Pair{0, 0};
+        Pair tot;
+        const Pair ex = block_excl_scan2(v, s_warp, &tot);
+        __syncthreads();
+        if (i < m) sums[i] = Pair{carry.a + ex.a, carry.b + ex.b};
+        carry.a += tot.a;
+        carry.b += tot.b;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) sums[m] = carry;
+}
+
+// active[slot] = v, fo[slot] = edge offset; fo[n_active] and count[0..1] = totals
+template <class OffT>
+__global__ void __launch_bounds__(SC_NT)
+    k_fscan_down(const uint8_t* __restrict__ mask, const OffT* __restrict__ off, int64_t n,
+                 const Pair* __restrict__ sums, int64_t nb, int32_t* __restrict__ active,
+                 int64_t* __restrict__ fo, int64_t* __restrict__ count) {
+    __shared__ Pair s_warp[SC_NT / 32];
+    const int64_t base = (int64_t)blockIdx.x * SC_TILE + (int64_t)threadIdx.x * SC_IPT;
+    Pair v[SC_IPT], t{0, 0};
+#pragma unroll
+    for (int k = 0; k < SC_IPT; ++k) {
+        v[k] = base + k < n ? frontier_item(mask, off, base + k) : Pair{0, 0};
+        t.a += v[k].a;
+        t.b += v[k].b;
+    }
+    const Pair ex = block_excl_scan2(t, s_warp, nullptr);
+    Pair run{sums[blockIdx.x].a + ex.a, sums[blockIdx.x].b + ex.b};
+#pragma unroll
+    for (int k = 0; k < SC_IPT; ++k) {
+        if (v[k].a) {
+            active[run.a] = (int32_t)(base + k);
+            fo[run.a] = run.b;
+        }
+        run.a += v[k].a;
+        run.b += v[k].b;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const Pair tot = sums[nb];
+        fo[tot.a] = tot.b;
+        count[0] = tot.a;
+        count[1] = tot.b;
+    }
+}
+
 // ---- relaxation ------------------------------------------------------------------------
 struct SsspOp {
     double* dist;
@@ -169,10 +279,27 @@ struct BfsOp {
     }
 };
 
+// Edges [e0, e1) of one source, four at a time: the column / weight loads and the
+// four atomics are all issued before any result is used, so a thread keeps
+// several relaxations in flight instead of one dependent round trip per edge.
 template <class OffT, class ValT, class Op>
 __device__ __forceinline__ void relax_edges(const Csr<OffT, ValT>& G, const Op& op, uint8_t* out,
                                             int64_t e0, int64_t e1, double du) {
-    for (int64_t e = e0; e < e1; ++e) {
+    constexpr int R = 4;
+    int64_t e = e0;
+    for (; e + R <= e1; e += R) {
+        int32_t v[R];
+        ValT w[R];
+        bool hit[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) { v[k] = __ldg(G.col + e + k); w[k] = __ldg(G.val + e + k); }
+#pragma unroll
+        for (int k = 0; k < R; ++k) hit[k] = op.relax(v[k], w[k], du);
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+            if (hit[k]) out[v[k]] = 1;
+    }
+    for (; e < e1; ++e) {
         const int64_t v = __ldg(G.col + e);
         const ValT w = __ldg(G.val + e);
         if (op.relax(v, w, du)) out[v] = 1;
@@ -244,14 +371,33 @@ __global__ void k_relax_group(Csr<OffT, ValT> G, Op op, const int32_t* __restric
         const int64_t tb = b * tpb, tc = min(tpb, n_active - tb);
         const int64_t base = fo[tb], tot = fo[tb + tc] - base;
         int64_t t = tb;
-        for (int64_t k = m; k < tot; k += members) {
-            const int64_t a = base + k;
-            while (fo[t + 1] <= a) ++t;
-            const int64_t u = active[t];
-            double du = 0.0;
-            op.prep(u, du);
-            const int64_t e = (int64_t)__ldg(G.off + u) + (a - fo[t]);
-            relax_edges(G, op, out, e, e + 1, du);
+        constexpr int R = 4;   // four member-stride atoms per round, relaxations in flight together
+        for (int64_t k0 = m; k0 < tot; k0 += R * members) {
+            int32_t v[R];
+            ValT w[R];
+            double du[R];
+            bool live[R], hit[R];
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                const int64_t a = base + k0 + q * members;
+                live[q] = k0 + q * members < tot;
+                v[q] = 0;
+                w[q] = (ValT)0;
+                du[q] = 0.0;
+                if (live[q]) {
+                    while (fo[t + 1] <= a) ++t;   // get_tile by monotone advance
+                    const int64_t u = active[t];
+                    op.prep(u, du[q]);
+                    const int64_t e = (int64_t)__ldg(G.off + u) + (a - fo[t]);
+                    v[q] = __ldg(G.col + e);
+                    w[q] = __ldg(G.val + e);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < R; ++q) hit[q] = live[q] && op.relax(v[q], w[q], du[q]);
+#pragma unroll
+            for (int q = 0; q < R; ++q)
+                if (hit[q]) out[v[q]] = 1;
         }
     }
 }
@@ -283,7 +429,7 @@ static size_t up256(size_t b) { return (b + 255) / 256 * 256; }
 
 size_t frontier_workspace(int64_t n) {
     const size_t nb = (size_t)scan_blocks(n) + 1;
-    return up256((size_t)n) * 2 + up256((size_t)n * 4) + up256((size_t)(n + 1) * 8) + up256(nb * 8) +
+    return up256((size_t)n) * 2 + up256((size_t)n * 4) + up256((size_t)(n + 1) * 8) + up256(nb * 16) +
            up256(16);
 }
 
@@ -294,7 +440,7 @@ static FrontierWs carve(void* ws, int64_t n) {
     w.mask_out = p; p += up256((size_t)n);
     w.active = (int32_t*)p; p += up256((size_t)n * 4);
     w.fo = (int64_t*)p; p += up256((size_t)(n + 1) * 8);
-    w.sums = (int64_t*)p; p += up256(((size_t)scan_blocks(n) + 1) * 8);
+    w.sums = (int64_t*)p; p += up256(((size_t)scan_blocks(n) + 1) * 16);
     w.count = (int64_t*)p;
     return w;
 }
@@ -313,7 +459,7 @@ static int64_t frontier_lanes(int schedule, int64_t n_active, int64_t atoms, int
             const int64_t cap = (int64_t)sm_count() * 2048;
             return n_active < cap ? (n_active > 0 ? n_active : 1) : cap;
         }
-        case LW_MERGE_PATH: return (n_active + atoms) > 0 ? ceil_div(n_active + atoms, 64) : 1;
+        case LW_MERGE_PATH: return (n_active + atoms) > 0 ? ceil_div(n_active + atoms, 16) : 1;
         default: return group_auto_lanes(n_active, gs, tpb);
     }
 }
@@ -403,23 +549,43 @@ static int traverse(const lw_csr_t* H, int64_t src, void* result, int schedule, 
     int64_t level = 0, np = 0;
     uint8_t* in = w.mask_in;
     uint8_t* out = w.mask_out;
+    const int64_t nb = scan_blocks(n);
+    Pair* sums = (Pair*)w.sums;
+    int64_t* hc = nullptr;   // pinned (n_active, atoms) read back once per pass
+    LW_TRY(cudaMallocHost((void**)&hc, 16));
+    int rc = LW_OK;
     for (;;) {
-        int rc = scan_run<FlagOf, true>(FlagOf{in}, n, w.sums, nullptr, w.active, w.count, s);
-        if (rc) return rc;
-        int64_t n_active = 0;
-        LW_TRY(cudaMemcpyAsync(&n_active, w.count, 8, cudaMemcpyDeviceToHost, s));
-        LW_TRY(cudaStreamSynchronize(s));
+        // one sweep: active[] = flatnonzero(in), fo[] = frontier edge offsets
+        if (H->offset_bits == 32) {
+            const int32_t* o = (const int32_t*)H->row_offsets;
+            k_fscan_up<int32_t><<<(unsigned)nb, SC_NT, 0, s>>>(in, o, n, sums);
+            k_fscan_sums<<<1, SC_NT, 0, s>>>(sums, nb);
+            k_fscan_down<int32_t><<<(unsigned)nb, SC_NT, 0, s>>>(in, o, n, sums, nb, w.active, w.fo, w.count);
+        } else {
+            const int64_t* o = (const int64_t*)H->row_offsets;
+            k_fscan_up<int64_t><<<(unsigned)nb, SC_NT, 0, s>>>(in, o, n, sums);
+            k_fscan_sums<<<1, SC_NT, 0, s>>>(sums, nb);
+            k_fscan_down<int64_t><<<(unsigned)nb, SC_NT, 0, s>>>(in, o, n, sums, nb, w.active, w.fo, w.count);
+        }
+        if ((rc = (int)cudaGetLastError())) break;
+        if ((rc = (int)cudaMemcpyAsync(hc, w.count, 16, cudaMemcpyDeviceToHost, s))) break;
+        if ((rc = (int)cudaStreamSynchronize(s))) break;
+        const int64_t n_active = hc[0], atoms = hc[1];
         if (n_active == 0) break;
-        rc = SSSP ? sssp_pass(H, w.active, n_active, (double*)result, out, schedule, lanes, gs, tpb, ws, s)
-                  : bfs_pass(H, w.active, n_active, (int64_t*)result, level + 1, out, schedule, lanes, gs,
-                             tpb, ws, s);
-        if (rc) return rc;
+        if ((rc = (int)cudaMemsetAsync(out, 0, (size_t)n, s))) break;
+        rc = SSSP ? relax_dispatch(H, SsspOp{(double*)result}, w.active, n_active, w.fo, atoms, out,
+                                   schedule, lanes, gs, tpb, s)
+                  : relax_dispatch(H, BfsOp{(int64_t*)result, level + 1}, w.active, n_active, w.fo, atoms,
+                                   out, schedule, lanes, gs, tpb, s);
+        if (rc) break;
         uint8_t* t = in;
         in = out;
         out = t;
         ++level;
         ++np;
     }
+    cudaFreeHost(hc);
+    if (rc) return rc;
     if (passes) *passes = np;
     return LW_OK;
 }
