@@ -29,7 +29,10 @@ namespace lw {
 
 // Chunk geometry shared by every dtype: a chunk is at most WO_S merge-path items
 // (rows + atoms) and its atoms sit in an 8-aligned window of WO_W atoms.
-constexpr int WO_W = 4096;
+#ifndef LW_WO_W
+#define LW_WO_W 4096
+#endif
+constexpr int WO_W = LW_WO_W;
 constexpr int WO_S = WO_W - 16;
 constexpr unsigned WO_PHASE_PARTITION = 1, WO_PHASE_SPMV = 2, WO_PHASE_FIXUP = 4;
 
@@ -637,9 +640,8 @@ static int launch_chunk(const Csr<OffT, ValT>& a, const ValT* x, ValT* y, const 
     static bool attr = false;   // one-time opt-in above the 48 KB default
     if (!attr) {
         LW_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-#ifdef LW_WO_CARVEOUT
-        LW_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, LW_WO_CARVEOUT));
-#endif
+        if (const char* cv = getenv("LW_WO_CARVEOUT"))   // A/B runs only
+            LW_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv)));
         attr = true;
     }
     kern<<<(unsigned)p.lanes, WoCfg<ValT>::NT, smem, s>>>(a, x, y, p.items, p.J, tiles, c_tile,
