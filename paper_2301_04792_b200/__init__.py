@@ -8,27 +8,28 @@ tiles) and ``spmv(m, x, cfg)``. The arithmetic runs in hand-written sm_100a
 kernels (liblwb200.so, C ABI in include/lw_b200.h); there is no CPU fallback.
 """
 
-from ._backend import (ENV_VAR, backend_name, cuda_active, cuda_available, numba_active,
-                       use_backend)
+from ._backend import (ENV_VAR, NUMBA_AVAILABLE, backend_name, cuda_active, cuda_available,
+                       numba_active, use_backend)
 from ._lib import BackendUnavailable
 from .device import (DeviceCsr, device_group_plan_prefix, device_merge_path_partition,
                      generate_banded_device, generate_rmat_csr)
-from .executor import (SENTINEL_TILE, AtomicMinArray, atomic_min_real, CarryOut, CarryPolicy, ExecutorConfig, ImbalanceReport,
-                       SUM_CARRIES, device_config, execute_merge_path, execute_tile_major,
-                       fixup_combine, imbalance)
+from .executor import (SENTINEL_TILE, SUM_CARRIES, AtomicMinArray, CarryOut, CarryPolicy,
+                       ExecutorConfig, ImbalanceReport, atomic_min_real, device_config,
+                       execute_merge_path, execute_tile_major, fixup_combine, imbalance)
 from .kernels import (HeuristicConfig, choose_spmv_schedule, spmm, spmv, spmv_auto,
                       spmv_probe)
-from .traversal import UNREACHED, SsspState, bfs, bfs_pass, device_graph, sssp, sssp_init, sssp_pass
+from .mmio import (MatrixMarketError, load_matrix_market, parse_matrix_market,
+                   write_matrix_market)
 from .schedules import (GroupMappedSchedule, GroupPlan, MergePathCoord, MergePathSchedule,
                         MergePathSlice, Schedule, ScheduleKind, ThreadMappedSchedule,
                         exclusive_prefix_sum, get_tile, group_plan, make_schedule,
                         merge_path_partition, merge_path_search, merge_path_slices, num_blocks,
                         thread_mapped_tiles)
-from .mmio import (MatrixMarketError, load_matrix_market, parse_matrix_market,
-                   write_matrix_market)
 from .sparse import (CooMatrix, CsrMatrix, Graph, coo_to_csr, csr_to_coo, generate_banded_csr,
                      generate_power_law_csr, generate_random_csr, rmat_thresholds,
                      row_length_stats, transpose_csr, validate_coo, validate_csr)
+from .traversal import (UNREACHED, SsspState, bfs, bfs_pass, device_graph, sssp, sssp_init,
+                        sssp_pass)
 from .work import (TileSet, csr_tile_set, infinite_range, lane_stride_range, step_range,
                    tile_offsets)
 
@@ -37,7 +38,7 @@ __version__ = "0.1.0"
 __all__ = [
     "AtomicMinArray", "SsspState", "UNREACHED", "atomic_min_real", "bfs", "bfs_pass",
     "device_graph", "sssp", "sssp_init", "sssp_pass",
-    "BackendUnavailable", "CarryOut", "CarryPolicy", "CooMatrix", "CsrMatrix", "Graph",
+    "BackendUnavailable", "NUMBA_AVAILABLE", "CarryOut", "CarryPolicy", "CooMatrix", "CsrMatrix", "Graph",
     "MatrixMarketError", "coo_to_csr", "csr_to_coo", "load_matrix_market", "parse_matrix_market",
     "transpose_csr", "validate_coo", "write_matrix_market", "DeviceCsr", "ENV_VAR",
     "ExecutorConfig", "GroupMappedSchedule", "GroupPlan", "HeuristicConfig", "ImbalanceReport",

@@ -16,6 +16,8 @@ from ._lib import BackendUnavailable
 
 ENV_VAR = "LWB200_BACKEND"
 _BACKENDS = ("cuda",)
+# reference name (_backend.py:17-22): there is no numba CPU backend in this package
+NUMBA_AVAILABLE = False
 
 
 def _resolve_default() -> str:

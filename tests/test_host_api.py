@@ -323,3 +323,26 @@ def test_atomic_min_array_semantics():
         a.atomic_min(0, -1.0)
     with pytest.raises(ValueError):
         lwb.AtomicMinArray(np.array([-1.0]))
+
+
+# the reference's public names (lanework/__init__.py:65-122), all of which must exist here
+REFERENCE_ALL = [
+    "AtomicMinArray", "CarryOut", "CarryPolicy", "CooMatrix", "CsrMatrix", "ExecutorConfig",
+    "Graph", "GroupPlan", "HeuristicConfig", "ImbalanceReport", "MatrixMarketError",
+    "MergePathCoord", "MergePathSlice", "NUMBA_AVAILABLE", "SENTINEL_TILE",
+    "ScheduleKind", "SsspState", "TileSet", "UNREACHED", "atomic_min_real", "backend_name", "bfs",
+    "choose_spmv_schedule", "coo_to_csr", "csr_tile_set", "csr_to_coo", "exclusive_prefix_sum",
+    "execute_merge_path", "execute_tile_major", "fixup_combine", "generate_power_law_csr",
+    "generate_random_csr", "get_tile", "group_plan", "imbalance", "infinite_range",
+    "lane_stride_range", "load_matrix_market", "merge_path_partition", "merge_path_search",
+    "merge_path_slices", "numba_active", "parse_matrix_market", "spmm", "spmv", "spmv_auto",
+    "sssp", "sssp_init", "sssp_pass", "step_range", "thread_mapped_tiles", "transpose_csr",
+    "use_backend", "validate_coo", "validate_csr", "write_matrix_market",
+]
+
+
+def test_reference_public_names_exist():
+    import paper_2301_04792_b200 as lwb
+
+    missing = [n for n in REFERENCE_ALL if not hasattr(lwb, n)]
+    assert not missing, missing
