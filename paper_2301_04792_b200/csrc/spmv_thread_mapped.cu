@@ -75,8 +75,10 @@ __device__ __forceinline__ double row_dot(const int32_t* __restrict__ col,
         // so a single thread keeps UV*V gathers in flight (the thread-mapped
         // schedule puts whole long rows on one thread)
         constexpr int UV = LW_TM_UV;
-        if (e - b >= 8 * UV * V)   // only long rows; short rows keep the plain loop below
-        for (; b + UV * V <= e; b += UV * V) {
+        if (e - b >= 8 * UV * V) {   // only long rows; short rows keep the plain loop below
+            // software pipeline: the next group's col_idx / values stream in
+            // while this group's gathers are in flight, so a step costs one
+            // round trip (the gathers) instead of two
             typename VT::ValV v[UV];
             typename VT::ColV c[UV];
 #pragma unroll
@@ -84,8 +86,22 @@ __device__ __forceinline__ double row_dot(const int32_t* __restrict__ col,
                 v[u] = __ldg(reinterpret_cast<const typename VT::ValV*>(val + b) + u);
                 c[u] = __ldg(reinterpret_cast<const typename VT::ColV*>(col + b) + u);
             }
+            for (; b + 2 * UV * V <= e; b += UV * V) {
+                typename VT::ValV vn[UV];
+                typename VT::ColV cn[UV];
+#pragma unroll
+                for (int u = 0; u < UV; ++u) {
+                    vn[u] = __ldg(reinterpret_cast<const typename VT::ValV*>(val + b + UV * V) + u);
+                    cn[u] = __ldg(reinterpret_cast<const typename VT::ColV*>(col + b + UV * V) + u);
+                }
+#pragma unroll
+                for (int u = 0; u < UV; ++u) accum_vec<ValT>(v[u], c[u], x, a0, a1);
+#pragma unroll
+                for (int u = 0; u < UV; ++u) { v[u] = vn[u]; c[u] = cn[u]; }
+            }
 #pragma unroll
             for (int u = 0; u < UV; ++u) accum_vec<ValT>(v[u], c[u], x, a0, a1);
+            b += UV * V;
         }
 #pragma unroll 2
         for (; b + V <= e; b += V) {

@@ -20,7 +20,8 @@ import numpy as np
 
 from . import _lib
 
-__all__ = ["DeviceCsr", "device_merge_path_partition", "device_group_plan_prefix",
+__all__ = ["DeviceCsr", "cached_device_csr", "drop_device_cache", "device_merge_path_partition",
+           "device_group_plan_prefix",
            "generate_rmat_csr", "generate_banded_device", "Workspace", "Probe", "current_stream"]
 
 
@@ -152,6 +153,35 @@ class DeviceCsr:
         sv = self.values.element_size()
         so = self.row_offsets.element_size()
         return self.nnz * (4 + sv) + (self.rows + 1) * so + self.cols * sv + self.rows * sv
+
+
+def cached_device_csr(m, dtype="float64", device=None) -> "DeviceCsr":
+    """Device copy of a host CsrMatrix, reused while its arrays are the same objects.
+
+    The reference's containers are immutable by convention (reference
+    sparse.py:1-7), so a host-API call (``spmv(m, x)`` with NumPy operands) need
+    not re-upload the matrix every time: the DeviceCsr is kept on the matrix and
+    reused while ``rows``, ``cols`` and the three arrays (identity, address,
+    length) are unchanged. Rebinding an array (``m.values = ...``) re-uploads;
+    mutating one in place is outside the contract — call
+    ``drop_device_cache(m)`` after doing so.
+    """
+    dev = _require_cuda(device)
+    arrays = (m.row_offsets, m.col_indices, m.values)
+    key = (int(m.rows), int(m.cols), str(_torch_dtype(dtype)), str(dev),
+           tuple((id(a), a.ctypes.data, a.shape[0]) for a in arrays))
+    cache = m.__dict__.setdefault("_lw_device_cache", {})
+    hit = cache.get(key[:4])
+    if hit is not None and hit[0] == key:
+        return hit[1]
+    d = DeviceCsr.from_host(m, dtype=dtype, device=dev)
+    cache[key[:4]] = (key, d)
+    return d
+
+
+def drop_device_cache(m) -> None:
+    """Forget the device copies cached on a host CsrMatrix (after in-place edits)."""
+    m.__dict__.pop("_lw_device_cache", None)
 
 
 class Workspace:

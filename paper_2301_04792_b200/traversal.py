@@ -24,7 +24,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _backend, _lib
-from .device import DeviceCsr, Workspace, current_stream
+from .device import DeviceCsr, Workspace, cached_device_csr, current_stream
 from .executor import ExecutorConfig
 from .kernels import schedule_code
 from .sparse import Graph
@@ -45,7 +45,7 @@ def device_graph(g, dtype="float64") -> DeviceCsr:
         return g
     if not isinstance(g, Graph):
         g = Graph(g)
-    return DeviceCsr.from_host(g.csr, dtype=dtype)
+    return cached_device_csr(g.csr, dtype=dtype)
 
 
 def _ws(G: DeviceCsr):

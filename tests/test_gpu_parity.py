@@ -367,3 +367,22 @@ def test_power_iteration_single_gpu_matches_oracle():
         xr = yr / ref_norms[-1]
     np.testing.assert_allclose(norms, ref_norms, rtol=1e-10)
     np.testing.assert_allclose(x.cpu().numpy(), xr, rtol=1e-9, atol=1e-12)
+
+
+def test_host_api_device_cache():
+    """Host-API calls reuse the matrix's device copy while its arrays are unchanged;
+    rebinding an array re-uploads; drop_device_cache forgets it."""
+    from paper_2301_04792_b200.device import cached_device_csr, drop_device_cache
+
+    m = lwb.generate_random_csr(200, 150, 2000, seed=3)
+    x = np.random.default_rng(1).random(m.cols)
+    y1 = lwb.spmv(m, x)
+    d1 = cached_device_csr(m)
+    assert cached_device_csr(m) is d1
+    m.values = m.values * 2.0                      # rebinding: new upload, new result
+    y2 = lwb.spmv(m, x)
+    assert cached_device_csr(m) is not d1
+    np.testing.assert_allclose(y2, 2.0 * y1, rtol=1e-12)
+    m.values[:] = m.values / 2.0                   # in-place edit: outside the contract
+    drop_device_cache(m)
+    np.testing.assert_allclose(lwb.spmv(m, x), y1, rtol=1e-12)
