@@ -58,7 +58,15 @@ def cuda_available() -> bool:
         return False
 
 
+_ready = False
+
+
 def require_cuda() -> None:
+    """Raise BackendUnavailable unless the library and a CUDA device are usable
+    (checked once; later calls are a flag test on the hot path)."""
+    global _ready
+    if _ready:
+        return
     if _active != "cuda":  # pragma: no cover - only one backend exists
         raise BackendUnavailable(f"backend {_active!r} is not the cuda backend")
     import torch
@@ -68,6 +76,7 @@ def require_cuda() -> None:
     from . import _lib
 
     _lib.load()
+    _ready = True
 
 
 @contextmanager

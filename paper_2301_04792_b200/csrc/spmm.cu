@@ -14,6 +14,8 @@
 // index and value once (the same address for the whole team, one L1 request)
 // and gathers a contiguous TS*VEC-wide row segment of B. Sums are fp64 and follow
 // the atom order of the reference loops, so integer data is bit-exact.
+#include <algorithm>
+
 #include "lw_common.cuh"
 
 namespace lw {
@@ -298,9 +300,14 @@ int64_t spmm_auto_lanes(int schedule, int64_t rows, int64_t nnz, int64_t n, int6
             return p < cap ? p : cap;
         }
         case LW_MERGE_PATH: {
+            // 256 items per lane on large inputs; smaller inputs get shorter lanes
+            // (down to 16 items) so that ~256 teams per SM still have work
             const int64_t total = rows + nnz;
-            const int64_t p = total > 0 ? ceil_div(total, mm_wo_items_target()) : 1;
-            return p;
+            if (total <= 0) return 1;
+            const int64_t teams = ((int64_t)sm_count() * 2048) >> lg;
+            const int64_t items = std::max<int64_t>(16, std::min<int64_t>(mm_wo_items_target(),
+                                                                          ceil_div(total, teams)));
+            return ceil_div(total, items);
         }
         default: return group_auto_lanes(rows, gs, tpb);
     }

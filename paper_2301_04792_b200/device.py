@@ -139,6 +139,16 @@ class DeviceCsr:
                          self.col_indices[a0:a1], self.values[a0:a1])
 
     def c_struct(self) -> _lib.LwCsr:
+        """The lw_csr_t view (cached while the three tensors are the same objects)."""
+        key = (id(self.row_offsets), id(self.col_indices), id(self.values), self.rows, self.cols)
+        hit = self.__dict__.get("_c_struct")
+        if hit is not None and hit[0] == key:
+            return hit[1]
+        s = self._make_c_struct()
+        self.__dict__["_c_struct"] = (key, s)
+        return s
+
+    def _make_c_struct(self) -> _lib.LwCsr:
         s = _lib.LwCsr()
         s.rows, s.cols, s.nnz = self.rows, self.cols, self.nnz
         s.row_offsets = self.row_offsets.data_ptr()
@@ -191,12 +201,10 @@ class Workspace:
         self._buf = {}
 
     def get(self, nbytes: int, device):
-        torch = _torch()
-        key = str(device)
-        buf = self._buf.get(key)
+        buf = self._buf.get(device)
         if buf is None or buf.numel() < nbytes:
-            buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
-            self._buf[key] = buf
+            buf = _torch().empty(max(nbytes, 256), dtype=_torch().uint8, device=device)
+            self._buf[device] = buf
         return buf
 
 

@@ -16,6 +16,7 @@ device size the lane count (see executor.device_config).
 
 from __future__ import annotations
 
+import functools
 from dataclasses import dataclass, replace
 
 import numpy as np
@@ -41,6 +42,16 @@ def _lanes_arg(cfg: ExecutorConfig) -> int:
     return 0 if cfg.lanes is None else int(cfg.lanes)
 
 
+@functools.lru_cache(maxsize=256)
+def _wo_workspace(rows: int, nnz: int, lanes: int, dtype_code: int) -> int:
+    return _lib.load().lw_spmv_work_oriented_workspace(rows, nnz, lanes, dtype_code)
+
+
+@functools.lru_cache(maxsize=256)
+def _mm_workspace(code: int, rows: int, nnz: int, n: int, lanes: int, dtype_code: int) -> int:
+    return _lib.load().lw_spmm_workspace(code, rows, nnz, n, lanes, dtype_code)
+
+
 def _launch(m: DeviceCsr, x, y, cfg: ExecutorConfig, probe: Probe | None, stream: int) -> None:
     lib = _lib.load()
     A = m.c_struct()
@@ -52,7 +63,7 @@ def _launch(m: DeviceCsr, x, y, cfg: ExecutorConfig, probe: Probe | None, stream
     if kind is ScheduleKind.THREAD_MAPPED:
         rc = lib.lw_spmv_thread_mapped(A, xp, yp, lanes, pp, stream)
     elif kind is ScheduleKind.MERGE_PATH:
-        need = lib.lw_spmv_work_oriented_workspace(m.rows, m.nnz, lanes, A.dtype)
+        need = _wo_workspace(m.rows, m.nnz, lanes, A.dtype)
         ws = _WS.get(need, m.device)
         rc = lib.lw_spmv_work_oriented(A, xp, yp, lanes, ws.data_ptr(), ws.numel(), pp, stream)
     else:
@@ -106,7 +117,7 @@ def _launch_spmm(m: DeviceCsr, B, C, cfg: ExecutorConfig, stream: int) -> None:
     lanes = _lanes_arg(cfg)
     bp = B.data_ptr() if B.numel() else None
     cp = C.data_ptr() if C.numel() else None
-    need = lib.lw_spmm_workspace(code, m.rows, m.nnz, n, lanes, A.dtype)
+    need = _mm_workspace(code, m.rows, m.nnz, n, lanes, A.dtype)
     ws = _WS.get(need, m.device) if need else None
     rc = lib.lw_spmm(code, A, bp, cp, n, lanes, cfg.group_size, cfg.tiles_per_block,
                      ws.data_ptr() if ws is not None else None, need, stream)
