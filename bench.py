@@ -427,6 +427,8 @@ def our_arm(args):
 
     # algorithmic bytes of the dominant kernel for this rank's shard
     alg_bytes = A.algorithmic_bytes()
+    sv = A.values.element_size()
+    gather_bytes = alg_bytes - A.cols * sv + A.nnz * sv
     hbm, hbm_src = peaks()
     achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
     workload = f"rmat{args.scale}-ef{args.edge_factor}-seed{args.seed}"
@@ -446,7 +448,10 @@ def our_arm(args):
                      "kernel": "k_wo_chunk" if sched is lwb.ScheduleKind.MERGE_PATH else args.schedule,
                      "kernel_ms": round(kern_ms, 4), "alg_bytes": alg_bytes,
                      "peak_source": hbm_src, "frac_of_8TBps": round(achieved / 8000.0, 4),
-                     "traffic_source": tr[1] if tr else None},
+                     "traffic_source": tr[1] if tr else None,
+                     # SURVEY §8(d) upper model: every atom gathers its own x value
+                     "achieved_gather_every_nnz": round(gather_bytes / (kern_ms * 1e-3) / 1e9, 1),
+                     "frac_gather_every_nnz": round(gather_bytes / (kern_ms * 1e-3) / 1e9 / hbm, 4)},
         "hbm_gbs_step": round(alg_bytes / (ms * 1e-3) / 1e9, 1),
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks.summary(),
