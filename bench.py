@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--mode", default="spmv", choices=["spmv", "power"],
                     help="spmv: one y=Ax per step (C3 headline); power: C5 power iteration")
     ap.add_argument("--iters", type=int, default=20, help="power iterations per step (C5)")
+    ap.add_argument("--fused", action="store_true",
+                    help="power mode: all-gather fused into the SpMV (peer/multicast row writes "
+                         "into symmetric-memory buffers) instead of NCCL")
     ap.add_argument("--chunks", type=int, default=0,
                     help="power mode: row chunks per shard whose all-gathers overlap the next "
                          "chunk's SpMV (0 = 4 when N > 1, else 1)")
@@ -265,8 +268,17 @@ def power_arm(args):
         spmv_ev.append((e0, e1))
         return yk
 
+    if args.fused:
+        from paper_2301_04792_b200.distributed import power_iteration_fused
+
+        def run_iters(k):
+            return power_iteration_fused(A, n, shard, k)
+    else:
+        def run_iters(k):
+            return power_iteration(local_spmv, n, shard, k, dtype=A.dtype, device=dev, chunks=chunks)
+
     for _ in range(max(args.warmup, 3)):
-        power_iteration(local_spmv, n, shard, 2, dtype=A.dtype, device=dev, chunks=chunks)
+        run_iters(2)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -276,8 +288,7 @@ def power_arm(args):
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record()
         for _ in range(args.steps):
-            x, norms = power_iteration(local_spmv, n, shard, args.iters, dtype=A.dtype, device=dev,
-                                       chunks=chunks)
+            x, norms = run_iters(args.iters)
         t1.record()
         torch.cuda.synchronize()
     if world > 1:
@@ -290,16 +301,18 @@ def power_arm(args):
         ms, spmv_ms = float(t[0]), float(t[1])
     gflops = 2.0 * nnz_total * args.iters / (ms * 1e-3) / 1e9
     line = {
-        "metric": f"power iteration GFLOP/s ({args.iters} iters, work_oriented SpMV + NCCL y all-gather)",
+        "metric": (f"power iteration GFLOP/s ({args.iters} iters, work_oriented SpMV "
+                   + ("with the y all-gather fused into its row writes)" if args.fused
+                      else "+ NCCL y all-gather)")),
         "value": round(gflops, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32" if args.dtype == "fp32" else "f64",
         "data": "synthetic",
         "config": {"workload": f"rmat{args.scale}-ef{args.edge_factor}-seed{args.seed}-power{args.iters}",
                    "rows": n, "nnz": nnz_total, "parallelism": f"rows{world}" if world > 1 else "single",
-                   "overlap_chunks": chunks},
-        "breakdown_ms": {"spmv_max_rank": round(spmv_ms, 3),
-                         "allgather_normalise": round(ms - spmv_ms, 3)},
+                   "overlap_chunks": 0 if args.fused else chunks, "fused_allgather": bool(args.fused)},
+        "breakdown_ms": None if args.fused else {"spmv_max_rank": round(spmv_ms, 3),
+                                                 "allgather_normalise": round(ms - spmv_ms, 3)},
         "final_norm": norms[-1] if norms else None,
         "gpu_launches": 3 * chunks * args.iters * args.steps,
         "clocks": clocks.summary(),

@@ -137,6 +137,20 @@ int lw_spmv_work_oriented_phases(const lw_csr_t* A, const void* x, void* y, int6
                                  void* workspace, size_t workspace_bytes,
                                  uint32_t phase_mask, uintptr_t stream);
 
+/* work_oriented SpMV fused with the all-gather of the power iteration (BASELINE
+ * C5): every row this rank's shard produces is written to y AND to
+ * element row_base + row of each rank's next-x buffer -- through the NVLS
+ * multicast address (multimem.st, one store reaches every GPU) when
+ * multicast_ptr != 0, else one peer-to-peer store per buffer in peer_ptrs
+ * (n_peers <= 8, HOST array of device addresses, e.g. symmetric-memory
+ * buffer_ptrs). Rows a lane boundary cuts are rewritten with their final value
+ * by the carry fix-up, so after a cross-GPU barrier every buffer holds the full
+ * y. Replaces SpMV + NCCL all-gather with one pass over NVLink. */
+int lw_spmv_work_oriented_peers(const lw_csr_t* A, const void* x, void* y, int64_t lanes,
+                                void* workspace, size_t workspace_bytes, int32_t n_peers,
+                                const uint64_t* peer_ptrs, uint64_t multicast_ptr,
+                                int64_t row_base, uintptr_t stream);
+
 /* group_mapped: groups of group_size lanes own blocks of tiles_per_block tiles,
  * members take block atoms by member stride (schedules.py:137-167,
  * executor.py:149-168). Replaces _fast.spmv_group_mapped (_fast.py:55-77).

@@ -21,6 +21,8 @@ int spmm(int, const lw_csr_t*, const void*, void*, int64_t, int64_t, int64_t, in
 int64_t spmm_auto_lanes(int schedule, int64_t rows, int64_t nnz, int64_t n, int64_t gs, int64_t tpb);
 size_t spmm_wo_workspace(int64_t lanes, int64_t n);
 size_t frontier_workspace(int64_t n);
+int spmv_work_oriented_peers(const lw_csr_t*, const void*, void*, int64_t, void*, size_t, int32_t,
+                             const uint64_t*, uint64_t, int64_t, cudaStream_t);
 int frontier_compact(const uint8_t*, int64_t, int32_t*, int64_t*, void*, cudaStream_t);
 int sssp_pass(const lw_csr_t*, const int32_t*, int64_t, double*, uint8_t*, int, int64_t, int64_t, int64_t, void*, cudaStream_t);
 int bfs_pass(const lw_csr_t*, const int32_t*, int64_t, int64_t*, int64_t, uint8_t*, int, int64_t, int64_t, int64_t, void*, cudaStream_t);
@@ -159,6 +161,19 @@ int lw_spmv_work_oriented_phases(const lw_csr_t* A, const void* x, void* y, int6
     if (A->nnz > 0 && !x) return LW_E_INVALID_ARG;
     if (lanes < 0 || phase_mask == 0 || phase_mask > 7u) return LW_E_INVALID_ARG;
     return spmv_work_oriented(A, x, y, lanes, ws, ws_bytes, nullptr, phase_mask, (cudaStream_t)stream);
+}
+
+int lw_spmv_work_oriented_peers(const lw_csr_t* A, const void* x, void* y, int64_t lanes,
+                                void* ws, size_t ws_bytes, int32_t n_peers,
+                                const uint64_t* peer_ptrs, uint64_t multicast_ptr,
+                                int64_t row_base, uintptr_t stream) {
+    int rc = check_csr(A);
+    if (rc) return rc;
+    if (A->rows > 0 && !y) return LW_E_INVALID_ARG;
+    if (A->nnz > 0 && !x) return LW_E_INVALID_ARG;
+    if (lanes < 0 || (n_peers == 0 && multicast_ptr == 0)) return LW_E_INVALID_ARG;
+    return spmv_work_oriented_peers(A, x, y, lanes, ws, ws_bytes, n_peers, peer_ptrs, multicast_ptr,
+                                    row_base, (cudaStream_t)stream);
 }
 
 int lw_spmv_group_mapped(const lw_csr_t* A, const void* x, void* y, int64_t lanes,

@@ -121,6 +121,36 @@ struct WoSmem {
     static constexpr size_t bytes = flag_off + sizeof(uint32_t) * (WO_W / 32 + 2);
 };
 
+// ---- fused all-gather output (power iteration over NVLink) -------------------------
+// Every row the SpMV produces is also stored into the next-x buffer of every rank:
+// either through the NVLS multicast address (one multimem.st reaches all GPUs on
+// the NVSwitch) or, without multicast, one P2P store per peer buffer. Row t of
+// this rank's shard lands at element base + t of each buffer.
+constexpr int LW_MAX_PEERS = 8;
+struct PeerOut {
+    int32_t n;                      // peer buffers (ignored when mc is set)
+    int64_t base;                   // global row of this shard's first row
+    uint64_t ptr[LW_MAX_PEERS];     // peer buffer base addresses (UVA, P2P-mapped)
+    uint64_t mc;                    // multicast base address, 0 = none
+};
+
+__device__ __forceinline__ void peer_store(const PeerOut& po, int64_t row, float v) {
+    if (po.mc) {
+        asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(po.mc + (uint64_t)(po.base + row) * 4),
+                     "f"(v) : "memory");
+        return;
+    }
+    for (int p = 0; p < po.n; ++p) reinterpret_cast<float*>(po.ptr[p])[po.base + row] = v;
+}
+__device__ __forceinline__ void peer_store(const PeerOut& po, int64_t row, double v) {
+    if (po.mc) {
+        asm volatile("multimem.st.relaxed.sys.global.f64 [%0], %1;" ::"l"(po.mc + (uint64_t)(po.base + row) * 8),
+                     "d"(v) : "memory");
+        return;
+    }
+    for (int p = 0; p < po.n; ++p) reinterpret_cast<double*>(po.ptr[p])[po.base + row] = v;
+}
+
 // 8 consecutive col_idx / values with 32-byte loads (sm_100 .v8.b32 / .v4.b64)
 __device__ __forceinline__ void ld8_col(const int32_t* p, int32_t* c) {
     const uint64_t pol = policy_evict_first();
@@ -199,11 +229,12 @@ __device__ __forceinline__ void store_run(double* dst, const double* v) {
     for (int h = 0; h < IPT / 2; ++h) d[h] = make_double2(v[2 * h], v[2 * h + 1]);
 }
 
-template <class OffT, class ValT, bool PROBE, bool VEC>
+template <class OffT, class ValT, bool PROBE, bool VEC, bool PEERS = false>
 __global__ void __launch_bounds__(WoCfg<ValT>::NT)
     k_wo_chunk(Csr<OffT, ValT> A, const ValT* __restrict__ x, ValT* __restrict__ y,
                int64_t items, int64_t J, const int64_t* __restrict__ bound_tile,
-               int64_t* __restrict__ carry_tile, double* __restrict__ carry_val, Probe probe) {
+               int64_t* __restrict__ carry_tile, double* __restrict__ carry_val, Probe probe,
+               PeerOut po = PeerOut{}) {
     constexpr int NT = WoCfg<ValT>::NT, IPT = WoCfg<ValT>::IPT;
     constexpr int W = WO_W, S = WO_S;
     static_assert(NT * IPT == W, "window must be NT*IPT atoms");
@@ -333,6 +364,7 @@ __global__ void __launch_bounds__(WoCfg<ValT>::NT)
             double v = e > st ? (double)s_seg[e - 1] : 0.0;
             if (i == 0 && run_has && run_row == t0) v += run_val;
             y[t0 + i] = (ValT)v;
+            if (PEERS) peer_store(po, t0 + i, (ValT)v);
         }
         if (PROBE) {
             for (int w = tid; w < n_atoms; w += NT) {
@@ -538,10 +570,10 @@ __global__ void __launch_bounds__(WoCfg<ValT>::NT)
 }
 
 // ---- 3. ordered carry fix-up -----------------------------------------------------
-template <class ValT>
+template <class ValT, bool PEERS = false>
 __global__ void k_carry_fixup(const int64_t* __restrict__ carry_tile,
                               const double* __restrict__ carry_val, int64_t n,
-                              ValT* __restrict__ y, int64_t rows) {
+                              ValT* __restrict__ y, int64_t rows, PeerOut po = PeerOut{}) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const int64_t r = carry_tile[k];
@@ -561,7 +593,9 @@ __global__ void k_carry_fixup(const int64_t* __restrict__ carry_tile,
         if (t != r) break;
         s += carry_val[m];
     }
-    y[r] = (ValT)((double)y[r] + s);
+    const ValT v = (ValT)((double)y[r] + s);
+    y[r] = v;
+    if (PEERS) peer_store(po, r, v);
 }
 
 // ---- host side -------------------------------------------------------------------
@@ -645,7 +679,7 @@ static int launch_chunk(const Csr<OffT, ValT>& a, const ValT* x, ValT* y, const 
         attr = true;
     }
     kern<<<(unsigned)p.lanes, WoCfg<ValT>::NT, smem, s>>>(a, x, y, p.items, p.J, tiles, c_tile,
-                                                         c_val, pr);
+                                                         c_val, pr, PeerOut{});
     LW_LAUNCH_CHECK();
     return LW_OK;
 }
@@ -727,6 +761,58 @@ static int launch_wo(const lw_csr_t* A, const void* x, void* y, const WoPlan& p,
         LW_LAUNCH_CHECK();
     }
     return LW_OK;
+}
+
+// SpMV whose rows also land in every rank's next-x buffer (fused all-gather).
+template <class OffT, class ValT>
+static int launch_wo_peers(const lw_csr_t* A, const void* x, void* y, const WoPlan& p, void* ws,
+                           const PeerOut& po, cudaStream_t s) {
+    Csr<OffT, ValT> a{A->rows, A->cols, A->nnz, (const OffT*)A->row_offsets, A->col_indices,
+                      (const ValT*)A->values};
+    const size_t nb = (size_t)(p.lanes * p.J + 1);
+    unsigned char* w = (unsigned char*)ws;
+    int64_t* tiles = (int64_t*)w;
+    int64_t* c_tile = (int64_t*)(w + align_up(nb * 8, 256));
+    double* c_val = (double*)(w + align_up(nb * 8, 256) + align_up(wo_carries(p) * 8, 256));
+    if (p.lanes > 0x7fffffff) return LW_E_UNSUPPORTED;
+    int rc = launch_search<OffT>(a.off, a.rows, a.nnz, (int64_t)nb, p.J, p.items, WO_S, tiles, nullptr, s);
+    if (rc) return rc;
+    const bool vec = ((uintptr_t)A->col_indices % 32 == 0) && ((uintptr_t)A->values % 32 == 0);
+    constexpr size_t smem = WoSmem<ValT>::bytes;
+    auto kern = vec ? k_wo_chunk<OffT, ValT, false, true, true> : k_wo_chunk<OffT, ValT, false, false, true>;
+    static bool attr[2] = {false, false};
+    if (!attr[vec]) {
+        LW_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr[vec] = true;
+    }
+    kern<<<(unsigned)p.lanes, WoCfg<ValT>::NT, smem, s>>>(a, (const ValT*)x, (ValT*)y, p.items, p.J,
+                                                         tiles, c_tile, c_val, Probe{}, po);
+    LW_LAUNCH_CHECK();
+    k_carry_fixup<ValT, true><<<ceil_div(p.lanes, 256), 256, 0, s>>>(c_tile, c_val, p.lanes, (ValT*)y,
+                                                                     a.rows, po);
+    LW_LAUNCH_CHECK();
+    return LW_OK;
+}
+
+int spmv_work_oriented_peers(const lw_csr_t* A, const void* x, void* y, int64_t lanes, void* ws,
+                             size_t ws_bytes, int32_t n_peers, const uint64_t* peer_ptrs,
+                             uint64_t mc_ptr, int64_t row_base, cudaStream_t s) {
+    if (n_peers < 0 || n_peers > LW_MAX_PEERS || (n_peers > 0 && !peer_ptrs) || row_base < 0)
+        return LW_E_INVALID_ARG;
+    const WoPlan p = wo_plan(A->rows, A->nnz, lanes);
+    if (A->rows == 0) return LW_OK;
+    if (!ws || ws_bytes < wo_workspace(A->rows, A->nnz, lanes)) return LW_E_WORKSPACE;
+    PeerOut po{};
+    po.n = n_peers;
+    po.base = row_base;
+    po.mc = mc_ptr;
+    for (int i = 0; i < n_peers; ++i) po.ptr[i] = peer_ptrs[i];
+    const bool o32 = A->offset_bits == 32;
+    if (A->dtype == LW_F32)
+        return o32 ? launch_wo_peers<int32_t, float>(A, x, y, p, ws, po, s)
+                   : launch_wo_peers<int64_t, float>(A, x, y, p, ws, po, s);
+    return o32 ? launch_wo_peers<int32_t, double>(A, x, y, p, ws, po, s)
+               : launch_wo_peers<int64_t, double>(A, x, y, p, ws, po, s);
 }
 
 int spmv_work_oriented(const lw_csr_t* A, const void* x, void* y, int64_t lanes, void* ws,

@@ -14,7 +14,8 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["nnz_balanced_bounds", "shard_of", "power_iteration", "chunk_bounds", "RowShard"]
+__all__ = ["nnz_balanced_bounds", "shard_of", "power_iteration", "power_iteration_fused",
+           "chunk_bounds", "RowShard"]
 
 
 def nnz_balanced_bounds(row_offsets, parts: int) -> np.ndarray:
@@ -146,4 +147,76 @@ def power_iteration(local_spmv, n: int, shard: RowShard, iters: int, group=None,
         x = torch.where(nrm > 0, y / nrm, y).to(x.dtype)
         if on_iter is not None:
             on_iter(k, x)
+    return x, [float(v) for v in norms]
+
+
+def _spmv_peers(A, x, y, peer_ptrs, mc_ptr: int, row_base: int, ws, stream: int) -> None:
+    import ctypes
+
+    from . import _lib
+
+    lib = _lib.load()
+    arr = (ctypes.c_uint64 * max(1, len(peer_ptrs)))(*[int(p) for p in peer_ptrs])
+    rc = lib.lw_spmv_work_oriented_peers(A.c_struct(), x.data_ptr(), y.data_ptr(), 0, ws.data_ptr(),
+                                         ws.numel(), len(peer_ptrs), arr, int(mc_ptr), row_base, stream)
+    _lib.check(rc, "lw_spmv_work_oriented_peers")
+
+
+def power_iteration_fused(A, n: int, shard: RowShard, iters: int, group=None, x0=None,
+                          multicast: bool = True):
+    """Power iteration with the all-gather fused into the SpMV (SURVEY §8(e) stretch).
+
+    ``A`` is this rank's row shard (DeviceCsr, rows [shard.r0, shard.r1)). The
+    next x lives in two symmetric-memory buffers (torch.distributed
+    _symmetric_memory: every rank's copy is mapped into every other rank's
+    address space over NVLink); the work_oriented SpMV kernel writes each row it
+    produces straight into all of them (lw_spmv_work_oriented_peers: one NVLS
+    multimem.st per row when the NVSwitch multicast object exists, else one P2P
+    store per peer), a device-side barrier on the buffer's signal pads orders
+    the writes before anyone reads, and every rank normalises its own full copy.
+    No NCCL call and no separate gather pass: the exchange rides on the SpMV's
+    own row writes. Buffers alternate between iterations, so one barrier per
+    iteration suffices (a rank rewrites a buffer only after every rank has
+    passed the barrier that follows its last read).
+
+    world == 1 runs the same kernel path with ordinary buffers (no peers).
+    Returns (x, norms) like power_iteration.
+    """
+    import torch
+    import torch.distributed as dist
+
+    from .device import Workspace, current_stream
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    dev, dtype = A.values.device, A.values.dtype
+    if world > 1:
+        import torch.distributed._symmetric_memory as symm_mem
+
+        g = group or dist.group.WORLD
+        bufs = [symm_mem.empty(n, dtype=dtype, device=dev) for _ in range(2)]
+        hdls = [symm_mem.rendezvous(b, g) for b in bufs]
+        peers = [list(h.buffer_ptrs) for h in hdls]
+        mcs = [int(getattr(h, "multicast_ptr", 0) or 0) if multicast else 0 for h in hdls]
+    else:
+        bufs = [torch.empty(n, dtype=dtype, device=dev) for _ in range(2)]
+        hdls = [None, None]
+        peers = [[b.data_ptr()] for b in bufs]
+        mcs = [0, 0]
+    x = torch.full((n,), 1.0 / np.sqrt(n), dtype=dtype, device=dev) if x0 is None else x0
+    y_local = torch.empty(max(A.rows, 1), dtype=dtype, device=dev)
+    from . import _lib
+
+    need = _lib.load().lw_spmv_work_oriented_workspace(A.rows, A.nnz, 0, A.c_struct().dtype)
+    ws = Workspace().get(need, dev)
+    stream = current_stream(dev)
+    norms = []
+    for k in range(iters):
+        b = k % 2
+        _spmv_peers(A, x, y_local, peers[b], mcs[b], shard.r0, ws, stream)
+        if hdls[b] is not None:
+            hdls[b].barrier(channel=0)
+        y = bufs[b]
+        nrm = torch.linalg.vector_norm(y, dtype=torch.float64)
+        norms.append(nrm)
+        x = torch.where(nrm > 0, y / nrm, y).to(dtype)
     return x, [float(v) for v in norms]

@@ -386,3 +386,48 @@ def test_host_api_device_cache():
     m.values[:] = m.values / 2.0                   # in-place edit: outside the contract
     drop_device_cache(m)
     np.testing.assert_allclose(lwb.spmv(m, x), y1, rtol=1e-12)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_fused_power_iteration_matches_nccl_driver(dtype):
+    """The SpMV-with-peer-writes path (world 1: the rank's own next-x buffer is
+    its only peer) gives exactly the iterates of the plain SpMV driver."""
+    from paper_2301_04792_b200.distributed import (RowShard, nnz_balanced_bounds, power_iteration,
+                                                   power_iteration_fused)
+
+    A = lwb.generate_rmat_csr(16, 8, seed=11, dtype="float32" if dtype == torch.float32 else "float64")
+    shard = RowShard(nnz_balanced_bounds(A.row_offsets.cpu().numpy(), 1), 0)
+    cfg = ExecutorConfig(schedule=ScheduleKind.MERGE_PATH)
+    x1, n1 = power_iteration(lambda x: lwb.spmv(A, x, cfg), A.rows, shard, 6, dtype=dtype,
+                             device="cuda")
+    x2, n2 = power_iteration_fused(A, A.rows, shard, 6)
+    torch.cuda.synchronize()
+    assert torch.equal(x1, x2)
+    assert n1 == n2
+
+
+def test_peers_kernel_writes_every_buffer_at_the_row_base():
+    """lw_spmv_work_oriented_peers: y plus every peer buffer get the shard's rows
+    at row_base; rows outside the shard are untouched."""
+    import ctypes
+
+    from paper_2301_04792_b200 import _lib
+
+    m = lwb.generate_power_law_csr(3000, 8.0, 1.2, seed=2)
+    A = m.to_device("float32")
+    x = torch.rand(A.cols, device="cuda")
+    want = lwb.spmv(A, x, ExecutorConfig(schedule=ScheduleKind.MERGE_PATH))
+    bufs = [torch.full((A.rows + 100,), -7.0, device="cuda") for _ in range(3)]
+    y = torch.empty(A.rows, device="cuda")
+    lib = _lib.load()
+    need = lib.lw_spmv_work_oriented_workspace(A.rows, A.nnz, 0, _lib.LW_F32)
+    ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+    ptrs = (ctypes.c_uint64 * 3)(*[b.data_ptr() for b in bufs])
+    rc = lib.lw_spmv_work_oriented_peers(A.c_struct(), x.data_ptr(), y.data_ptr(), 0, ws.data_ptr(),
+                                         need, 3, ptrs, 0, 60, torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    torch.cuda.synchronize()
+    assert torch.equal(y, want)
+    for b in bufs:
+        assert torch.equal(b[60:60 + A.rows], want)
+        assert (b[:60] == -7.0).all() and (b[60 + A.rows:] == -7.0).all()
