@@ -314,7 +314,7 @@ def power_arm(args):
         "breakdown_ms": None if args.fused else {"spmv_max_rank": round(spmv_ms, 3),
                                                  "allgather_normalise": round(ms - spmv_ms, 3)},
         "final_norm": norms[-1] if norms else None,
-        "gpu_launches": 3 * chunks * args.iters * args.steps,
+        "gpu_launches": (3 * (1 if args.fused else chunks) + 3) * args.iters * args.steps,
         "clocks": clocks.summary(),
     }
     if rank == 0:

@@ -151,6 +151,17 @@ int lw_spmv_work_oriented_peers(const lw_csr_t* A, const void* x, void* y, int64
                                 const uint64_t* peer_ptrs, uint64_t multicast_ptr,
                                 int64_t row_base, uintptr_t stream);
 
+/* Power-iteration normalisation (BASELINE C5; the reference driver's x = y/||y||):
+ * lw_vector_norm writes ||y||_2 (fp64, deterministic two-level reduction) to the
+ * DEVICE scalar norm_out; lw_vector_scale writes x = y / norm (x = y when the
+ * norm is 0) reading the device scalar, so the pair runs without a host sync.
+ * Workspace: lw_norm_workspace(n) bytes of device memory. */
+size_t lw_norm_workspace(int64_t n);
+int lw_vector_norm(const void* y, int64_t n, int32_t dtype, void* workspace,
+                   size_t workspace_bytes, double* norm_out, uintptr_t stream);
+int lw_vector_scale(const void* y, int64_t n, int32_t dtype, const double* norm, void* x_out,
+                    uintptr_t stream);
+
 /* group_mapped: groups of group_size lanes own blocks of tiles_per_block tiles,
  * members take block atoms by member stride (schedules.py:137-167,
  * executor.py:149-168). Replaces _fast.spmv_group_mapped (_fast.py:55-77).

@@ -30,6 +30,7 @@ SOURCES = [
     "spmv_group_mapped.cu",
     "spmm.cu",
     "frontier.cu",
+    "vector_ops.cu",
     "generators.cu",
     "mmio.cpp",
 ]

@@ -41,6 +41,9 @@ EXPORTS = (
     "lw_spmv_work_oriented",
     "lw_spmv_work_oriented_phases",
     "lw_spmv_work_oriented_peers",
+    "lw_norm_workspace",
+    "lw_vector_norm",
+    "lw_vector_scale",
     "lw_spmv_group_mapped",
     "lw_spmv_workspace",
     "lw_spmv",
@@ -129,6 +132,9 @@ _SIGNATURES = {
     "lw_spmv_work_oriented_phases": (ctypes.c_int, [_csr_p, _vp, _vp, _i64, _vp, _sz, _u32, _up]),
     "lw_spmv_work_oriented_peers": (ctypes.c_int, [_csr_p, _vp, _vp, _i64, _vp, _sz, _i32, _vp, _u64,
                                                    _i64, _up]),
+    "lw_norm_workspace": (_sz, [_i64]),
+    "lw_vector_norm": (ctypes.c_int, [_vp, _i64, _i32, _vp, _sz, _vp, _up]),
+    "lw_vector_scale": (ctypes.c_int, [_vp, _i64, _i32, _vp, _vp, _up]),
     "lw_spmv_group_mapped": (ctypes.c_int, [_csr_p, _vp, _vp, _i64, _i64, _i64, _probe_p, _up]),
     "lw_spmv_workspace": (_sz, [ctypes.c_int, _i64, _i64, _i64, _i32]),
     "lw_spmv": (ctypes.c_int, [ctypes.c_int, _csr_p, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _up]),

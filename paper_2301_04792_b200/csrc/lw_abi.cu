@@ -21,6 +21,9 @@ int spmm(int, const lw_csr_t*, const void*, void*, int64_t, int64_t, int64_t, in
 int64_t spmm_auto_lanes(int schedule, int64_t rows, int64_t nnz, int64_t n, int64_t gs, int64_t tpb);
 size_t spmm_wo_workspace(int64_t lanes, int64_t n);
 size_t frontier_workspace(int64_t n);
+size_t norm_workspace(int64_t n);
+int vector_norm(const void*, int64_t, int, void*, double*, cudaStream_t);
+int vector_scale(const void*, int64_t, int, const double*, void*, cudaStream_t);
 int spmv_work_oriented_peers(const lw_csr_t*, const void*, void*, int64_t, void*, size_t, int32_t,
                              const uint64_t*, uint64_t, int64_t, cudaStream_t);
 int frontier_compact(const uint8_t*, int64_t, int32_t*, int64_t*, void*, cudaStream_t);
@@ -310,6 +313,25 @@ int lw_spmm_group_mapped(const lw_csr_t* A, const void* B, void* C, int64_t n, i
 int lw_spmm(int schedule, const lw_csr_t* A, const void* B, void* C, int64_t n, int64_t lanes,
             int64_t gs, int64_t tpb, void* ws, size_t ws_bytes, uintptr_t stream) {
     return spmm_entry(schedule, A, B, C, n, lanes, gs, tpb, ws, ws_bytes, stream);
+}
+
+/* ---- power-iteration normalisation ----------------------------------------------------- */
+
+size_t lw_norm_workspace(int64_t n) { return n < 0 ? 0 : norm_workspace(n); }
+
+int lw_vector_norm(const void* y, int64_t n, int32_t dtype, void* ws, size_t ws_bytes,
+                   double* norm_out, uintptr_t stream) {
+    if (n < 0 || (n > 0 && !y) || !norm_out || (dtype != LW_F32 && dtype != LW_F64))
+        return LW_E_INVALID_ARG;
+    if (!ws || ws_bytes < norm_workspace(n)) return LW_E_WORKSPACE;
+    return vector_norm(y, n, dtype, ws, norm_out, (cudaStream_t)stream);
+}
+
+int lw_vector_scale(const void* y, int64_t n, int32_t dtype, const double* norm, void* x_out,
+                    uintptr_t stream) {
+    if (n < 0 || (n > 0 && (!y || !x_out)) || !norm || (dtype != LW_F32 && dtype != LW_F64))
+        return LW_E_INVALID_ARG;
+    return vector_scale(y, n, dtype, norm, x_out, (cudaStream_t)stream);
 }
 
 /* ---- SSSP / BFS ------------------------------------------------------------------------ */

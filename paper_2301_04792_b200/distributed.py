@@ -141,13 +141,56 @@ def power_iteration(local_spmv, n: int, shard: RowShard, iters: int, group=None,
             y = torch.cat(recvs).index_select(0, order)
         else:
             y = torch.cat([local_spmv(x, int(mine[c]), int(mine[c + 1])) for c in range(chunks)])
-        # ||y|| accumulated in fp64 on the device; no host sync inside the loop
-        nrm = torch.linalg.vector_norm(y, dtype=torch.float64)
+        # ||y|| in fp64 and x = y / ||y|| on the device; no host sync inside the loop
+        nrm, x = _normalise(y, x.dtype)
         norms.append(nrm)
-        x = torch.where(nrm > 0, y / nrm, y).to(x.dtype)
         if on_iter is not None:
             on_iter(k, x)
     return x, [float(v) for v in norms]
+
+
+def _normalise(y, dtype):
+    """(||y||_2 as a device fp64 scalar, y / ||y||): the library's deterministic
+    norm + scale kernels for CUDA tensors (one read for the norm, one read + write
+    for the scaling), torch for CPU tensors (the gloo tests)."""
+    import torch
+
+    if not y.is_cuda:
+        nrm = torch.linalg.vector_norm(y, dtype=torch.float64)
+        return nrm, torch.where(nrm > 0, y / nrm, y).to(dtype)
+    from . import _lib
+    from .device import _dtype_code, current_stream
+
+    lib = _lib.load()
+    y = y.contiguous()
+    code = _dtype_code(y.dtype)
+    need = lib.lw_norm_workspace(y.numel())
+    ws = _NORM_WS.get(max(need, 8), y.device)
+    nrm = torch.empty((), dtype=torch.float64, device=y.device)
+    stream = current_stream(y.device)
+    _lib.check(lib.lw_vector_norm(y.data_ptr(), y.numel(), code, ws.data_ptr(), ws.numel(),
+                                  nrm.data_ptr(), stream), "lw_vector_norm")
+    x = torch.empty_like(y, dtype=dtype)
+    if x.dtype != y.dtype:
+        return nrm, torch.where(nrm > 0, y / nrm, y).to(dtype)
+    _lib.check(lib.lw_vector_scale(y.data_ptr(), y.numel(), code, nrm.data_ptr(), x.data_ptr(),
+                                   stream), "lw_vector_scale")
+    return nrm, x
+
+
+class _LazyWs:
+    def __init__(self):
+        self._ws = None
+
+    def get(self, nbytes, device):
+        if self._ws is None:
+            from .device import Workspace
+
+            self._ws = Workspace()
+        return self._ws.get(nbytes, device)
+
+
+_NORM_WS = _LazyWs()
 
 
 def _spmv_peers(A, x, y, peer_ptrs, mc_ptr: int, row_base: int, ws, stream: int) -> None:
@@ -215,8 +258,6 @@ def power_iteration_fused(A, n: int, shard: RowShard, iters: int, group=None, x0
         _spmv_peers(A, x, y_local, peers[b], mcs[b], shard.r0, ws, stream)
         if hdls[b] is not None:
             hdls[b].barrier(channel=0)
-        y = bufs[b]
-        nrm = torch.linalg.vector_norm(y, dtype=torch.float64)
+        nrm, x = _normalise(bufs[b], dtype)
         norms.append(nrm)
-        x = torch.where(nrm > 0, y / nrm, y).to(dtype)
     return x, [float(v) for v in norms]

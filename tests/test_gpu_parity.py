@@ -431,3 +431,23 @@ def test_peers_kernel_writes_every_buffer_at_the_row_base():
     for b in bufs:
         assert torch.equal(b[60:60 + A.rows], want)
         assert (b[:60] == -7.0).all() and (b[60 + A.rows:] == -7.0).all()
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_device_normalisation(dtype):
+    """lw_vector_norm / lw_vector_scale: ||y|| within fp64 rounding of a sorted
+    fp64 sum, run-to-run identical, x = y/||y||; y = 0 stays 0."""
+    from paper_2301_04792_b200.distributed import _normalise
+
+    g = torch.Generator(device="cuda").manual_seed(3)
+    y = torch.randn(3_000_001, generator=g, device="cuda", dtype=dtype)
+    n1, x1 = _normalise(y, dtype)
+    n2, x2 = _normalise(y, dtype)
+    assert torch.equal(n1, n2) and torch.equal(x1, x2)
+    want = np.sqrt(np.sum(np.sort(y.double().cpu().numpy() ** 2)))
+    assert abs(float(n1) - want) <= 1e-12 * want
+    np.testing.assert_allclose(x1.double().cpu().numpy(), y.double().cpu().numpy() / want,
+                               rtol=1e-6 if dtype == torch.float32 else 1e-14)
+    z = torch.zeros(1000, device="cuda", dtype=dtype)
+    nz, xz = _normalise(z, dtype)
+    assert float(nz) == 0.0 and torch.equal(xz, z)
