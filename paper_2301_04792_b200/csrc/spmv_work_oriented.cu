@@ -400,175 +400,6 @@ __global__ void __launch_bounds__(WoCfg<ValT>::NT)
     }
 }
 
-// ---- 2w. warp-autonomous chunk kernel ------------------------------------------------
-// One CTA per chunk (lane), one __syncthreads per chunk. The CTA streams the
-// chunk's atoms (32-byte loads), issues every gather, stages the chunk's row
-// ends in shared memory, and synchronises once. From there each warp works
-// alone on its WARP_ATOMS-atom slice of the window: it derives its segment-head
-// bits from the staged row ends, runs the segmented scan with shuffles, writes
-// the rows that end inside its slice, and emits a carry for the row its slice
-// ends in. Carries are indexed (chunk, warp), so they are ordered along the
-// merge path and k_carry_fixup adds them exactly like the lane carries of the
-// reference (kernels.py:90-91). The merge-path partition (the schedule) stays at
-// chunk granularity; the per-warp cut inside a chunk is a reduction detail.
-template <class OffT, class ValT, bool PROBE, bool VEC>
-__global__ void __launch_bounds__(WoCfg<ValT>::NT)
-    k_wo_warp(Csr<OffT, ValT> A, const ValT* __restrict__ x, ValT* __restrict__ y,
-              int64_t items, int64_t J, const int64_t* __restrict__ bound_tile,
-              int64_t* __restrict__ carry_tile, double* __restrict__ carry_val, Probe probe) {
-    constexpr int NT = WoCfg<ValT>::NT, IPT = WoCfg<ValT>::IPT;
-    constexpr int NW = NT / kWarp, W = WO_W, S = WO_S;
-    extern __shared__ __align__(16) unsigned char sm[];
-    int32_t* s_end = reinterpret_cast<int32_t*>(sm);                      // [S]
-    ValT* s_run = reinterpret_cast<ValT*>(sm + sizeof(int32_t) * S);      // [W] running sums
-
-    const int tid = threadIdx.x, lane = tid & (kWarp - 1), warp = tid >> 5;
-    const int64_t l = blockIdx.x;
-    const int64_t total = A.rows + A.nnz;
-    const int pos = IPT * tid;                 // window position of my first atom
-    const int wlo = IPT * kWarp * warp;        // my warp's slice [wlo, whi)
-    const int whi = wlo + IPT * kWarp;
-
-    for (int64_t jc = 0; jc < J; ++jc) {
-        const int64_t b = l * J + jc;
-        const int64_t d0 = min(l * items + min(jc * S, items), total);
-        const int64_t d1 = min(l * items + min((jc + 1) * S, items), total);
-        if (d0 >= d1) {
-            if (lane == 0) { carry_tile[b * NW + warp] = -1; carry_val[b * NW + warp] = 0.0; }
-            continue;
-        }
-        const int64_t t0 = bound_tile[b], t1 = bound_tile[b + 1];
-        const int64_t a0 = d0 - t0;
-        const int n_rows = (int)(t1 - t0), n_atoms = (int)((d1 - t1) - a0);
-        const int64_t base = a0 & ~(int64_t)7;
-        const int w0 = (int)(a0 - base), w1 = w0 + n_atoms;
-        if (PROBE && probe.lane_atoms && tid == 0) probe.lane_atoms[l] += n_atoms;
-
-        // ---- loads: atoms, gathers, row ends ----
-        const int64_t g = base + pos;
-        ValT p[IPT];
-        {
-            int32_t c[IPT];
-            ValT v[IPT];
-#pragma unroll
-            for (int k = 0; k < IPT; ++k) { c[k] = 0; v[k] = (ValT)0; }
-            if (pos < w1) {
-                if (VEC && g + IPT <= A.nnz) {
-                    ld_atoms<IPT>(A.col + g, A.val + g, c, v);
-                } else {
-#pragma unroll
-                    for (int k = 0; k < IPT; ++k)
-                        if (g + k < A.nnz) { c[k] = ld_stream(A.col + g + k); v[k] = ld_stream(A.val + g + k); }
-                }
-            }
-            for (int i = tid; i < n_rows; i += NT)
-                s_end[i] = (int32_t)(ld_off(A.off + t0 + 1 + i) - base);
-#pragma unroll
-            for (int k = 0; k < IPT; ++k) {
-                const bool in = pos + k >= w0 && pos + k < w1;
-                p[k] = in ? v[k] * ld_gather(x + c[k]) : (ValT)0;
-            }
-        }
-        __syncthreads();   // row ends staged
-
-        // ---- my row ends: first row end >= pos (ends are nondecreasing) ----
-        int i_lo = 0;
-        {
-            int hi = n_rows;
-            while (i_lo < hi) {
-                const int mid = (i_lo + hi) >> 1;
-                if (s_end[mid] < pos) i_lo = mid + 1;
-                else hi = mid;
-            }
-        }
-        // head bits: a row end e in [pos, pos+IPT) starts a new segment at atom e
-        uint32_t fl = 0;
-        int i = i_lo;
-        for (; i < n_rows; ++i) {
-            const int e = s_end[i];
-            if (e >= pos + IPT) break;
-            fl |= 1u << (e - pos);
-        }
-        // ---- warp segmented scan (never crosses the warp's slice) ----
-        bool has = fl != 0u;
-        ValT run = (ValT)0;
-#pragma unroll
-        for (int k = 0; k < IPT; ++k) run = ((fl >> k) & 1u) ? p[k] : run + p[k];
-#pragma unroll
-        for (int d = 1; d < kWarp; d <<= 1) {
-            const ValT ov = shfl_up(run, d);
-            const int oh = shfl_up((int)has, d);
-            if (lane >= d) {
-                if (!has) run += ov;
-                has = has || oh;
-            }
-        }
-        // carry into my atoms: the previous lane's inclusive running sum
-        ValT r = shfl_up(run, 1);
-        if (lane == 0) r = (ValT)0;
-#pragma unroll
-        for (int k = 0; k < IPT; ++k) {
-            r = ((fl >> k) & 1u) ? p[k] : r + p[k];
-            s_run[pos + k] = r;
-        }
-        __syncwarp();
-
-        // ---- rows whose last atom lies in my IPT atoms (e in (pos, pos+IPT]) ----
-        {
-            int k = i_lo;
-            // rows ending exactly at pos belong to the previous thread, except
-            // the very first thread, which also owns rows ending at or before it
-            if (tid != 0)
-                while (k < n_rows && s_end[k] <= pos) ++k;
-            for (; k < n_rows; ++k) {
-                const int e = s_end[k];
-                if (e > pos + IPT) break;
-                const int st = k ? s_end[k - 1] : w0;
-                const ValT v = e > st ? s_run[e - 1] : (ValT)0;
-                y[t0 + k] = v;
-            }
-        }
-        if (PROBE) {
-#pragma unroll
-            for (int k = 0; k < IPT; ++k) {
-                const int wp = pos + k;
-                if (wp >= w0 && wp < w1) {
-                    int lo = 0, hi = n_rows;
-                    while (lo < hi) {
-                        const int mid = (lo + hi) >> 1;
-                        if (s_end[mid] <= wp) lo = mid + 1;
-                        else hi = mid;
-                    }
-                    probe_atom(probe, base + wp, l, t0 + lo);
-                }
-            }
-        }
-        // ---- the warp's carry: the open segment at its last atom ----
-        if (lane == kWarp - 1) {
-            const int last = min(whi, w1) - 1;   // last atom position of the slice
-            int64_t ct = -1;
-            double cv = 0.0;
-            if (last >= max(wlo, w0)) {
-                // row of atom `last`: number of row ends <= last
-                int lo = 0, hi = n_rows;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (s_end[mid] <= last) lo = mid + 1;
-                    else hi = mid;
-                }
-                const bool open = lo == n_rows || s_end[lo] > last + 1;
-                if (open) {
-                    ct = t0 + lo;
-                    cv = (double)s_run[last];
-                }
-            }
-            carry_tile[b * NW + warp] = (ct >= 0 && ct < A.rows) ? ct : -1;
-            carry_val[b * NW + warp] = cv;
-        }
-        __syncthreads();   // s_end / s_run are rewritten by the next chunk
-    }
-}
-
 // ---- 3. ordered carry fix-up -----------------------------------------------------
 template <class ValT, bool PEERS = false>
 __global__ void k_carry_fixup(const int64_t* __restrict__ carry_tile,
@@ -615,9 +446,8 @@ static WoPlan wo_plan(int64_t rows, int64_t nnz, int64_t lanes) {
 
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-// carry slots: one per (chunk, warp) for the warp kernel (the largest layout)
-constexpr int WO_MAX_NW = 16;
-static size_t wo_carries(const WoPlan& p) { return (size_t)(p.lanes * p.J) * WO_MAX_NW; }
+// carry slots: one per lane
+static size_t wo_carries(const WoPlan& p) { return (size_t)p.lanes; }
 
 size_t wo_workspace(int64_t rows, int64_t nnz, int64_t lanes) {
     const WoPlan p = wo_plan(rows, nnz, lanes);
@@ -684,26 +514,9 @@ static int launch_chunk(const Csr<OffT, ValT>& a, const ValT* x, ValT* y, const 
     return LW_OK;
 }
 
-template <class Kern>
-static int set_smem(Kern kern, size_t smem, bool& done) {
-    if (!done) {   // one-time opt-in above the 48 KB default
-        LW_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        done = true;
-    }
-    return LW_OK;
-}
-
-// Kernel variant for the SpMV phase: 'c' (default) k_wo_chunk, 'v' k_wo_warp.
-// LW_WO_KERNEL overrides it for A/B runs (DESIGN.md records the measurements).
-static char wo_kind() {
-    static const char* e = getenv("LW_WO_KERNEL");
-    return (e && e[0] == 'v') ? 'v' : 'c';
-}
-
 template <class OffT, class ValT>
 static int launch_wo(const lw_csr_t* A, const void* x, void* y, const WoPlan& p, void* ws,
                      const lw_probe_t* probe, unsigned phases, cudaStream_t s) {
-    constexpr int NT = WoCfg<ValT>::NT, NW = NT / kWarp;
     Csr<OffT, ValT> a{A->rows, A->cols, A->nnz, (const OffT*)A->row_offsets,
                       A->col_indices, (const ValT*)A->values};
     const size_t nb = (size_t)(p.lanes * p.J + 1), nc = wo_carries(p);
@@ -716,9 +529,7 @@ static int launch_wo(const lw_csr_t* A, const void* x, void* y, const WoPlan& p,
     if (p.lanes > 0x7fffffff) return LW_E_UNSUPPORTED;
     // 32-byte vector loads need 32-byte aligned col_idx / values
     const bool vec = ((uintptr_t)A->col_indices % 32 == 0) && ((uintptr_t)A->values % 32 == 0);
-    const char kind = wo_kind();
-    // carries the fix-up walks: (chunk, warp) for 'v', lanes otherwise
-    const int64_t n_carry = kind == 'v' ? (int64_t)(nb - 1) * NW : p.lanes;
+    const int64_t n_carry = p.lanes;   // the fix-up walks one carry per lane
 
     if (phases & WO_PHASE_PARTITION) {
         int rc = launch_search<OffT>(a.off, a.rows, a.nnz, (int64_t)nb, p.J, p.items, WO_S, tiles,
@@ -731,28 +542,10 @@ static int launch_wo(const lw_csr_t* A, const void* x, void* y, const WoPlan& p,
         ValT* yv = (ValT*)y;
         const bool P = probe != nullptr;
         int rc = LW_OK;
-        switch (kind) {
-            case 'c':
-                if (P) rc = vec ? launch_chunk<OffT, ValT, true, true>(a, xv, yv, p, tiles, c_tile, c_val, pr, s)
-                                : launch_chunk<OffT, ValT, true, false>(a, xv, yv, p, tiles, c_tile, c_val, pr, s);
-                else   rc = vec ? launch_chunk<OffT, ValT, false, true>(a, xv, yv, p, tiles, c_tile, c_val, pr, s)
-                                : launch_chunk<OffT, ValT, false, false>(a, xv, yv, p, tiles, c_tile, c_val, pr, s);
-                break;
-            default: {
-                constexpr size_t smem = sizeof(int32_t) * WO_S + sizeof(ValT) * WO_W;
-                static bool done[4];
-                const int idx = (P ? 2 : 0) + (vec ? 1 : 0);
-#define LW_WOV(PR, VEC)                                                                              \
-    {                                                                                                \
-        auto kern = k_wo_warp<OffT, ValT, PR, VEC>;                                                  \
-        if ((rc = set_smem(kern, smem, done[idx]))) return rc;                                       \
-        kern<<<(unsigned)p.lanes, NT, smem, s>>>(a, xv, yv, p.items, p.J, tiles, c_tile, c_val, pr); \
-    }
-                if (P) { if (vec) LW_WOV(true, true) else LW_WOV(true, false) }
-                else   { if (vec) LW_WOV(false, true) else LW_WOV(false, false) }
-#undef LW_WOV
-            }
-        }
+        if (P) rc = vec ? launch_chunk<OffT, ValT, true, true>(a, xv, yv, p, tiles, c_tile, c_val, pr, s)
+                        : launch_chunk<OffT, ValT, true, false>(a, xv, yv, p, tiles, c_tile, c_val, pr, s);
+        else   rc = vec ? launch_chunk<OffT, ValT, false, true>(a, xv, yv, p, tiles, c_tile, c_val, pr, s)
+                        : launch_chunk<OffT, ValT, false, false>(a, xv, yv, p, tiles, c_tile, c_val, pr, s);
         if (rc) return rc;
         LW_LAUNCH_CHECK();
     }
