@@ -195,16 +195,19 @@ def drop_device_cache(m) -> None:
 
 
 class Workspace:
-    """Grow-only device scratch buffer (per device), reused across launches."""
+    """Grow-only device scratch buffers, one per (device, stream), reused across
+    launches: calls on one stream are ordered, so they may share a buffer; calls
+    on different streams get different buffers and can run concurrently."""
 
     def __init__(self):
         self._buf = {}
 
-    def get(self, nbytes: int, device):
-        buf = self._buf.get(device)
+    def get(self, nbytes: int, device, stream: int = 0):
+        key = (device, stream)
+        buf = self._buf.get(key)
         if buf is None or buf.numel() < nbytes:
             buf = _torch().empty(max(nbytes, 256), dtype=_torch().uint8, device=device)
-            self._buf[device] = buf
+            self._buf[key] = buf
         return buf
 
 

@@ -165,9 +165,9 @@ def _normalise(y, dtype):
     y = y.contiguous()
     code = _dtype_code(y.dtype)
     need = lib.lw_norm_workspace(y.numel())
-    ws = _NORM_WS.get(max(need, 8), y.device)
-    nrm = torch.empty((), dtype=torch.float64, device=y.device)
     stream = current_stream(y.device)
+    ws = _NORM_WS.get(max(need, 8), y.device, stream)
+    nrm = torch.empty((), dtype=torch.float64, device=y.device)
     _lib.check(lib.lw_vector_norm(y.data_ptr(), y.numel(), code, ws.data_ptr(), ws.numel(),
                                   nrm.data_ptr(), stream), "lw_vector_norm")
     x = torch.empty_like(y, dtype=dtype)
@@ -182,12 +182,12 @@ class _LazyWs:
     def __init__(self):
         self._ws = None
 
-    def get(self, nbytes, device):
+    def get(self, nbytes, device, stream=0):
         if self._ws is None:
             from .device import Workspace
 
             self._ws = Workspace()
-        return self._ws.get(nbytes, device)
+        return self._ws.get(nbytes, device, stream)
 
 
 _NORM_WS = _LazyWs()

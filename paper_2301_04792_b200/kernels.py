@@ -64,7 +64,7 @@ def _launch(m: DeviceCsr, x, y, cfg: ExecutorConfig, probe: Probe | None, stream
         rc = lib.lw_spmv_thread_mapped(A, xp, yp, lanes, pp, stream)
     elif kind is ScheduleKind.MERGE_PATH:
         need = _wo_workspace(m.rows, m.nnz, lanes, A.dtype)
-        ws = _WS.get(need, m.device)
+        ws = _WS.get(need, m.device, stream)
         rc = lib.lw_spmv_work_oriented(A, xp, yp, lanes, ws.data_ptr(), ws.numel(), pp, stream)
     else:
         rc = lib.lw_spmv_group_mapped(A, xp, yp, lanes, cfg.group_size, cfg.tiles_per_block, pp,
@@ -118,7 +118,7 @@ def _launch_spmm(m: DeviceCsr, B, C, cfg: ExecutorConfig, stream: int) -> None:
     bp = B.data_ptr() if B.numel() else None
     cp = C.data_ptr() if C.numel() else None
     need = _mm_workspace(code, m.rows, m.nnz, n, lanes, A.dtype)
-    ws = _WS.get(need, m.device) if need else None
+    ws = _WS.get(need, m.device, stream) if need else None
     rc = lib.lw_spmm(code, A, bp, cp, n, lanes, cfg.group_size, cfg.tiles_per_block,
                      ws.data_ptr() if ws is not None else None, need, stream)
     _lib.check(rc, f"spmm[{cfg.schedule.value}]")

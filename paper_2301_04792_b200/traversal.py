@@ -50,7 +50,7 @@ def device_graph(g, dtype="float64") -> DeviceCsr:
 
 def _ws(G: DeviceCsr):
     need = _lib.load().lw_frontier_workspace(G.rows)
-    return _WS.get(need, G.device), need
+    return _WS.get(need, G.device, current_stream(G.device)), need
 
 
 def _cfg_args(cfg: ExecutorConfig):

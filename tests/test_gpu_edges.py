@@ -90,3 +90,25 @@ def test_mmio_special_values_roundtrip_to_device():
     csr = lwb.coo_to_csr(coo)
     y = lwb.spmv(csr, np.array([1.0, 1.0, 0.0]))
     assert y[0] == 1e-300 and y[1] == -2.5e10 and np.isinf(y[2])
+
+
+def test_concurrent_streams_use_separate_workspaces():
+    """work_oriented SpMV / SpMM on two streams at once (each stream gets its own
+    workspace): both results match the single-stream ones."""
+    rng = np.random.default_rng(12)
+    mats = [integer_csr(rng, 20_000, 20_000, 400_000), integer_csr(rng, 30_000, 25_000, 300_000)]
+    A = [dev(m, "float32") for m in mats]
+    xs = [torch.as_tensor(rng.integers(-2, 3, size=a.cols).astype(np.float32), device="cuda") for a in A]
+    cfg = ExecutorConfig(schedule=ScheduleKind.MERGE_PATH)
+    want = [lwb.spmv(a, x, cfg) for a, x in zip(A, xs)]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [[], []]
+    for _ in range(20):
+        for k in range(2):
+            with torch.cuda.stream(streams[k]):
+                outs[k].append(lwb.spmv(A[k], xs[k], cfg))
+    torch.cuda.synchronize()
+    for k in range(2):
+        for y in outs[k]:
+            assert torch.equal(y, want[k])
