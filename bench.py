@@ -65,6 +65,8 @@ def parse():
     ap.add_argument("--mode", default="spmv", choices=["spmv", "power"],
                     help="spmv: one y=Ax per step (C3 headline); power: C5 power iteration")
     ap.add_argument("--iters", type=int, default=20, help="power iterations per step (C5)")
+    ap.add_argument("--graph", action="store_true",
+                    help="power mode: capture the iterations once into a CUDA graph and replay it")
     ap.add_argument("--fused", action="store_true",
                     help="power mode: all-gather fused into the SpMV (peer/multicast row writes "
                          "into symmetric-memory buffers) instead of NCCL")
@@ -268,7 +270,20 @@ def power_arm(args):
         spmv_ev.append((e0, e1))
         return yk
 
-    if args.fused:
+    if args.graph:
+        from paper_2301_04792_b200.distributed import power_iteration_graph
+
+        def plain_spmv(x):
+            lwb.spmv(A, x, cfg, out=y_local)
+            return y_local
+
+        graphs = {}
+
+        def run_iters(k):
+            if k not in graphs:
+                graphs[k] = power_iteration_graph(plain_spmv, n, shard, k, dtype=A.dtype, device=dev)
+            return graphs[k]()
+    elif args.fused:
         from paper_2301_04792_b200.distributed import power_iteration_fused
 
         def run_iters(k):
@@ -310,8 +325,9 @@ def power_arm(args):
         "data": "synthetic",
         "config": {"workload": f"rmat{args.scale}-ef{args.edge_factor}-seed{args.seed}-power{args.iters}",
                    "rows": n, "nnz": nnz_total, "parallelism": f"rows{world}" if world > 1 else "single",
-                   "overlap_chunks": 0 if args.fused else chunks, "fused_allgather": bool(args.fused)},
-        "breakdown_ms": None if args.fused else {"spmv_max_rank": round(spmv_ms, 3),
+                   "overlap_chunks": 0 if (args.fused or args.graph) else chunks,
+                   "fused_allgather": bool(args.fused), "cuda_graph": bool(args.graph)},
+        "breakdown_ms": None if (args.fused or args.graph) else {"spmv_max_rank": round(spmv_ms, 3),
                                                  "allgather_normalise": round(ms - spmv_ms, 3)},
         "final_norm": norms[-1] if norms else None,
         "gpu_launches": (3 * (1 if args.fused else chunks) + 3) * args.iters * args.steps,

@@ -93,7 +93,7 @@ def test_mmio_special_values_roundtrip_to_device():
 
 
 def test_concurrent_streams_use_separate_workspaces():
-    """work_oriented SpMV / SpMM on two streams at once (each stream gets its own
+    """work_oriented SpMV on two streams at once (each stream gets its own
     workspace): both results match the single-stream ones."""
     rng = np.random.default_rng(12)
     mats = [integer_csr(rng, 20_000, 20_000, 400_000), integer_csr(rng, 30_000, 25_000, 300_000)]

@@ -451,3 +451,25 @@ def test_device_normalisation(dtype):
     z = torch.zeros(1000, device="cuda", dtype=dtype)
     nz, xz = _normalise(z, dtype)
     assert float(nz) == 0.0 and torch.equal(xz, z)
+
+
+def test_power_iteration_graph_replay_matches_eager():
+    """The CUDA-graph-captured power iteration replays the exact eager iterates."""
+    from paper_2301_04792_b200.distributed import (RowShard, nnz_balanced_bounds, power_iteration,
+                                                   power_iteration_graph)
+
+    A = lwb.generate_rmat_csr(15, 8, seed=5)
+    shard = RowShard(nnz_balanced_bounds(A.row_offsets.cpu().numpy(), 1), 0)
+    cfg = ExecutorConfig(schedule=ScheduleKind.MERGE_PATH)
+    y = torch.empty(A.rows, dtype=A.dtype, device="cuda")
+
+    def spmv(x):
+        lwb.spmv(A, x, cfg, out=y)
+        return y
+
+    x1, n1 = power_iteration(spmv, A.rows, shard, 7, dtype=A.dtype, device="cuda")
+    run = power_iteration_graph(spmv, A.rows, shard, 7, dtype=A.dtype, device="cuda")
+    for _ in range(2):
+        x2, n2 = run()
+        torch.cuda.synchronize()
+        assert torch.equal(x1, x2) and n1 == n2
