@@ -245,23 +245,39 @@ __global__ void __launch_bounds__(MM_NT)
     const int64_t members = min(gs, lanes - g * gs);
     const int64_t blocks = (A.rows + tpb - 1) / tpb;
     const int64_t sw = ((int64_t)VEC) << lg_ts;
-    for (int64_t b = g; b < blocks; b += groups) {
-        const int64_t tb = b * tpb, tc = min(tpb, A.rows - tb);
-        const int64_t base = (int64_t)__ldg(A.off + tb), tot = (int64_t)__ldg(A.off + tb + tc) - base;
-        int64_t t = tb;
-        for (int64_t k = m; k < tot; k += members) {
-            const int64_t a = base + k;
-            while ((int64_t)__ldg(A.off + t + 1) <= a) ++t;   // get_tile by monotone advance
-            const double v = (double)__ldg(A.val + a);
-            const int64_t src = __ldg(A.col + a);
-            for (int64_t cs = 0; cs < n; cs += sw) {
-                const int64_t c = cs + (int64_t)tl * VEC;
-                if (c >= n) continue;
-                ValT bv[VEC];
-                ld_row<ValT, VEC>(B + src * n + c, bv);
+    // Slabs outermost: a member's consecutive atoms usually stay in one tile, so its
+    // products are summed in registers and added to C once per tile run (the
+    // atomics of the reference's C[tile] += v*B[src] are per run, not per atom).
+    for (int64_t cs = 0; cs < n; cs += sw) {
+        const int64_t c = cs + (int64_t)tl * VEC;
+        if (c >= n) continue;
+        for (int64_t b = g; b < blocks; b += groups) {
+            const int64_t tb = b * tpb, tc = min(tpb, A.rows - tb);
+            const int64_t base = (int64_t)__ldg(A.off + tb), tot = (int64_t)__ldg(A.off + tb + tc) - base;
+            int64_t t = tb, cur = -1;
+            double acc[VEC];
 #pragma unroll
-                for (int j = 0; j < VEC; ++j) atomic_add_out(C + t * n + c + j, v * (double)bv[j]);
+            for (int j = 0; j < VEC; ++j) acc[j] = 0.0;
+            for (int64_t k = m; k < tot; k += members) {
+                const int64_t a = base + k;
+                while ((int64_t)__ldg(A.off + t + 1) <= a) ++t;   // get_tile by monotone advance
+                if (t != cur) {
+                    if (cur >= 0)
+#pragma unroll
+                        for (int j = 0; j < VEC; ++j) atomic_add_out(C + cur * n + c + j, acc[j]);
+                    cur = t;
+#pragma unroll
+                    for (int j = 0; j < VEC; ++j) acc[j] = 0.0;
+                }
+                const double v = (double)__ldg(A.val + a);
+                ValT bv[VEC];
+                ld_row<ValT, VEC>(B + (int64_t)__ldg(A.col + a) * n + c, bv);
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) acc[j] = fma(v, (double)bv[j], acc[j]);
             }
+            if (cur >= 0)
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) atomic_add_out(C + cur * n + c + j, acc[j]);
         }
     }
 }
