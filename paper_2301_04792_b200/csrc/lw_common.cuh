@@ -179,6 +179,23 @@ __device__ __forceinline__ double warp_segsum_to_head(double v, int key, int lan
     return v;
 }
 
+// Same result shape from a ballot of segment heads (keys nondecreasing across
+// lanes, head = first lane of a run): each level moves one value (one SHFL for
+// fp32 partials, two for fp64) instead of the value and the key, and the run
+// boundary comes from the head mask instead of key compares.
+template <class R>
+__device__ __forceinline__ R warp_segsum_heads(R v, int lane, uint32_t heads) {
+    // last lane of my run: the lane before the next head above me (or 31)
+    const uint32_t above = heads & ~((2u << lane) - 1u);   // heads strictly above lane
+    const int seg_end = above ? (__ffs(above) - 2) : (kWarp - 1);
+#pragma unroll
+    for (int d = 1; d < kWarp; d <<= 1) {
+        const R ov = __shfl_down_sync(0xffffffffu, v, d);
+        if (lane + d <= seg_end) v += ov;
+    }
+    return v;
+}
+
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 int sm_count();  // cached per device (lw_abi.cu)

@@ -12,10 +12,11 @@
 // Kernels (replace _fast.spmv_group_mapped, _fast.py:55-77):
 //  * k_group_warp   (group_size = tiles_per_block = 32): a warp is a group. The
 //    block plan is a warp-shuffle exclusive scan of the 32 per-tile atom counts;
-//    atom -> tile is a 5-probe binary search over that prefix done with shuffles;
-//    each 32-atom step is reduced with a shuffle segmented reduction keyed on tile
-//    and the run heads add into a per-warp shared accumulator, so y is written
-//    once per tile, coalesced, with a fixed summation order.
+//    atom -> tile (get_tile) follows the tile starts that fall inside each 32-atom
+//    step (a ballot over the plan, one shuffle per start); each step is reduced
+//    with a ballot-driven shuffle segmented reduction and the run heads add into a
+//    per-warp shared accumulator, so y is written once per tile, coalesced, with
+//    a fixed summation order.
 //  * k_group_block<NT> (group_size = tiles_per_block = NT in {64,128,256}): the
 //    CTA is a group; the plan is a block-wide scan into shared memory, atom ->
 //    tile is a log2(NT)-probe search in shared memory, per-warp shared
@@ -120,6 +121,7 @@ __global__ void __launch_bounds__(256)
         // U member-stride steps per iteration (lane takes local atoms k0+u*32+lane),
         // all their loads and gathers in flight before the first reduction; U = GU
         // only for long blocks (short ones would waste the padded steps)
+        int t_cur = 0;   // tile of the previous step's last atom (warp-uniform)
         auto steps = [&](auto uc) {
           constexpr int U = decltype(uc)::value;
           StepLoads<ValT, U> cur, nxt;
@@ -133,24 +135,49 @@ __global__ void __launch_bounds__(256)
             } else {
                 gather_steps<ValT, U, kWarp>(A, x, base, k0, lane, total, p);
             }
+            // non-empty tiles starting inside this step's atoms (lane j <-> tile j)
+            const uint32_t starts = U == 1 ? __ballot_sync(
+                0xffffffffu, lane < tc && cnt > 0 && excl >= k0 && excl < k0 + (OffT)kWarp) : 0u;
+            const int t_it = t_cur;
+            int t_next = t_cur;
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const OffT k = k0 + u * kWarp + lane;
                 const bool valid = k < total;
-                // get_tile: largest t < tc with excl[t] <= k (empty tiles never win)
+                // get_tile (largest non-empty t with excl[t] <= k): the step's atoms
+                // are consecutive, so only the non-empty tiles that START inside the
+                // step can change the tile; lane j flags tile j, and the few flagged
+                // starts are broadcast in order (one shuffle each, none inside a
+                // long row) instead of a 5-probe search per atom
+                // (long blocks, U > 1, keep the independent 5-probe search: there the
+                // steps' searches overlap, and R-MAT / power-law blocks measured 15-25%
+                // slower with the start-following loop)
                 int t = 0;
+                if (U == 1) {
+                    t = t_it;
+                    for (uint32_t sm = starts; sm; sm &= sm - 1) {
+                        const int j = __ffs(sm) - 1;
+                        if (k >= shfl(excl, j)) t = j;
+                    }
+                    t_next = shfl(t, kWarp - 1);
+                } else {
 #pragma unroll
-                for (int s = kWarp / 2; s >= 1; s >>= 1) {
-                    const OffT e = shfl(excl, t + s);
-                    if (t + s < tc && e <= k) t += s;
+                    for (int s = kWarp / 2; s >= 1; s >>= 1) {
+                        const OffT e = shfl(excl, t + s);
+                        if (t + s < tc && e <= k) t += s;
+                    }
                 }
                 if (PROBE && valid) { probe_atom(probe, base + k, glane, tb + t); ++mine; }
                 const int key = valid ? t : INT_MAX;
-                const double sum = warp_segsum_to_head(p[u], key, lane);
                 const int prev = shfl_up(key, 1);
-                if (valid && (lane == 0 || prev != key)) s_acc[warp][t] += sum;
+                const bool head = lane == 0 || prev != key;
+                const uint32_t heads = __ballot_sync(0xffffffffu, head);
+                // a step's partial sums (<= 32 products) in the value precision
+                const double sum = (double)warp_segsum_heads<ValT>((ValT)p[u], lane, heads);
+                if (valid && head) s_acc[warp][t] += sum;
                 __syncwarp();
             }
+            t_cur = t_next;
           }
         };
         if (total >= (OffT)(GU_LONG * kWarp)) steps(std::integral_constant<int, GU>{});
@@ -216,9 +243,12 @@ __global__ void __launch_bounds__(NT)
                 }
                 if (PROBE && valid) { probe_atom(probe, base + k, glane, tb + t); ++mine; }
                 const int key = valid ? t : INT_MAX;
-                const double sum = warp_segsum_to_head(p[u], key, lane);
                 const int prev = shfl_up(key, 1);
-                if (valid && (lane == 0 || prev != key)) s_acc[warp][t] += sum;
+                const bool head = lane == 0 || prev != key;
+                const uint32_t heads = __ballot_sync(0xffffffffu, head);
+                // a step's partial sums (<= 32 products) in the value precision
+                const double sum = (double)warp_segsum_heads<ValT>((ValT)p[u], lane, heads);
+                if (valid && head) s_acc[warp][t] += sum;
                 __syncwarp();
             }
           }
