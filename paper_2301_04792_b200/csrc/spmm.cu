@@ -40,21 +40,22 @@ __device__ __forceinline__ void ld_row(const ValT* p, ValT* v) {
         v[0] = __ldg(p);
     }
 }
-template <class ValT, int VEC>
-__device__ __forceinline__ void st_row(ValT* p, const double* a) {
+template <class ValT, int VEC, class AccT = double>
+__device__ __forceinline__ void st_row(ValT* p, const AccT* a) {
     if constexpr (VEC == 4) {
         *reinterpret_cast<float4*>(p) = make_float4((float)a[0], (float)a[1], (float)a[2], (float)a[3]);
     } else if constexpr (VEC == 2) {
-        *reinterpret_cast<double2*>(p) = make_double2(a[0], a[1]);
+        *reinterpret_cast<double2*>(p) = make_double2((double)a[0], (double)a[1]);
     } else {
         p[0] = (ValT)a[0];
     }
 }
 
 // atoms per batch of the atom-major walk: about 16 B-row values per thread in flight
+// (16-byte vectors: 4 atoms; fp64 with 8 atoms spilled and was 25-33% slower)
 template <int VEC>
 struct MmU {
-    static constexpr int U = VEC >= 4 ? 4 : 8;
+    static constexpr int U = VEC >= 2 ? 4 : 8;
 };
 
 // Accumulate atoms [a, a+cnt) (cnt <= MM_U, all in the same row) into acc.
@@ -154,10 +155,19 @@ __global__ void __launch_bounds__(MM_NT, LW_MM_WO_MINB)
         int64_t t = t0;
         int64_t re = t < t1 ? (int64_t)__ldg(A.off + t + 1) : a1;
         int64_t re2 = t + 1 < t1 ? (int64_t)__ldg(A.off + t + 2) : a1;
+        // fp32: products are summed in fp32 within a batch of U atoms and folded
+        // into the fp64 row sum once per batch (4 fp32 FMAs per fp64 add: -23%
+        // time on C3 n=16 against fp64 FMAs for every product); fp64 sums directly
+        constexpr bool kBatchPart = sizeof(ValT) == 4;
         double acc[VEC];
+        ValT part[VEC];
 #pragma unroll
-        for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
+        for (int v = 0; v < VEC; ++v) { acc[v] = 0.0; part[v] = (ValT)0; }
         auto finish_row = [&]() {
+            if constexpr (kBatchPart) {
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) { acc[v] += (double)part[v]; part[v] = (ValT)0; }
+            }
             if (active) st_row<ValT, VEC>(C + t * n + c, acc);
 #pragma unroll
             for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
@@ -186,9 +196,18 @@ __global__ void __launch_bounds__(MM_NT, LW_MM_WO_MINB)
             for (int k = 0; k < U; ++k) {
                 if (k < cnt) {
                     while (t < t1 && re <= a + k) finish_row();
+                    if constexpr (kBatchPart) {
 #pragma unroll
-                    for (int v = 0; v < VEC; ++v) acc[v] = fma((double)val[k], (double)b[k][v], acc[v]);
+                        for (int v = 0; v < VEC; ++v) part[v] = fma(val[k], b[k][v], part[v]);
+                    } else {
+#pragma unroll
+                        for (int v = 0; v < VEC; ++v) acc[v] = fma((double)val[k], (double)b[k][v], acc[v]);
+                    }
                 }
+            }
+            if constexpr (kBatchPart) {
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) { acc[v] += (double)part[v]; part[v] = (ValT)0; }
             }
         }
         while (t < t1) finish_row();   // rows ending at a1, and empty rows
