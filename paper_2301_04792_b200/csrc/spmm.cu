@@ -53,6 +53,7 @@ __device__ __forceinline__ void st_row(ValT* p, const AccT* a) {
 
 // atoms per batch of the atom-major walk: about 16 B-row values per thread in flight
 // (16-byte vectors: 4 atoms; fp64 with 8 atoms spilled and was 25-33% slower)
+// (6 or 8 atoms with fp32 vectors spilled: 31-39% slower)
 template <int VEC>
 struct MmU {
     static constexpr int U = VEC >= 2 ? 4 : 8;
@@ -78,10 +79,24 @@ __device__ __forceinline__ void mm_batch(const Csr<OffT, ValT>& A, const ValT* _
 #pragma unroll
             for (int j = 0; j < VEC; ++j) b[k][j] = (ValT)0;
     }
+    if constexpr (sizeof(ValT) == 4) {
+        // fp32: the batch is summed in fp32 and folded into the fp64 sum once
+        // (an fp64 FMA per product was 28-34% slower on C2u)
+        ValT part[VEC];
 #pragma unroll
-    for (int k = 0; k < MM_U; ++k)
+        for (int j = 0; j < VEC; ++j) part[j] = (ValT)0;
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) acc[j] = fma((double)val[k], (double)b[k][j], acc[j]);
+        for (int k = 0; k < MM_U; ++k)
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) part[j] = fma(val[k], b[k][j], part[j]);
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) acc[j] += (double)part[j];
+    } else {
+#pragma unroll
+        for (int k = 0; k < MM_U; ++k)
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) acc[j] = fma((double)val[k], (double)b[k][j], acc[j]);
+    }
 }
 
 // Full sum of atoms [s, e) for one slab (sequential in atom order).
