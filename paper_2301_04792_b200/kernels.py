@@ -95,7 +95,8 @@ def spmv(m, x, cfg: ExecutorConfig | None = None, *, out=None, dtype=None):
     if isinstance(m, DeviceCsr):
         x = _check_device_x(m, x)
         y = out if out is not None else torch.empty(m.rows, dtype=m.dtype, device=m.device)
-        if y.shape != (m.rows,) or y.dtype != m.dtype or y.device != m.device:
+        if (y.shape != (m.rows,) or y.dtype != m.dtype or y.device != m.device
+                or not y.is_contiguous()):
             raise ValueError("out must be a contiguous vector of length rows with the matrix dtype")
         _launch(m, x, y, cfg, None, current_stream(m.device))
         return y
@@ -147,7 +148,8 @@ def spmm(m, B, cfg: ExecutorConfig | None = None, *, out=None, dtype=None):
         B = B.contiguous()
         C = out if out is not None else torch.empty((m.rows, B.shape[1]), dtype=m.dtype,
                                                     device=m.device)
-        if C.shape != (m.rows, B.shape[1]) or C.dtype != m.dtype or not C.is_contiguous():
+        if (C.shape != (m.rows, B.shape[1]) or C.dtype != m.dtype or C.device != m.device
+                or not C.is_contiguous()):
             raise ValueError("out must be a contiguous [rows, k] tensor with the matrix dtype")
         _launch_spmm(m, B, C, cfg, current_stream(m.device))
         return C

@@ -112,3 +112,19 @@ def test_concurrent_streams_use_separate_workspaces():
     for k in range(2):
         for y in outs[k]:
             assert torch.equal(y, want[k])
+
+
+def test_out_buffers_are_validated():
+    """out= must be a contiguous buffer of the right shape, dtype and device."""
+    m = lwb.generate_random_csr(50, 40, 300, seed=2)
+    A = dev(m, "float32")
+    x = torch.ones(40, dtype=torch.float32, device="cuda")
+    with pytest.raises(ValueError):
+        lwb.spmv(A, x, out=torch.empty(100, dtype=torch.float32, device="cuda")[::2])
+    with pytest.raises(ValueError):
+        lwb.spmv(A, x, out=torch.empty(50, dtype=torch.float64, device="cuda"))
+    B = torch.ones(40, 3, dtype=torch.float32, device="cuda")
+    with pytest.raises(ValueError):
+        lwb.spmm(A, B, out=torch.empty(3, 50, dtype=torch.float32, device="cuda").t())
+    y = lwb.spmv(A, x, out=torch.empty(50, dtype=torch.float32, device="cuda"))
+    np.testing.assert_allclose(y.cpu().numpy(), lwb.spmv(m, np.ones(40)), rtol=1e-5, atol=1e-5)
