@@ -489,9 +489,25 @@ def our_arm(args):
     # e2e through the C ABI with HOST x and y (pinned), copies inside the timed
     # region; the matrix is the resident operator (uploaded once, like weights).
     # e2e_cold additionally uploads the whole CSR every call (lw_spmv_host).
-    if not args.no_e2e and world == 1:
-        line["e2e"] = e2e_resident(A, args, lib, dev, nnz_total)
-        line["e2e_cold"] = e2e_host(A, args, lib, dev, nnz_total)
+    # At N > 1 every rank runs the same loop on its shard (full x in, its rows of
+    # y out); the job's time is the slowest rank's and the bytes are summed.
+    if not args.no_e2e:
+        barrier()
+        e2e = e2e_resident(A, args, lib, dev, nnz_total)
+        if world > 1:
+            t = torch.tensor([e2e["ms_per_step"], e2e["h2d_bytes_per_step"],
+                              e2e["d2h_bytes_per_step"]], dtype=torch.float64, device=dev)
+            tmax, tsum = t.clone(), t.clone()
+            dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+            dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+            e2e_ms = float(tmax[0])
+            e2e.update({"value": round(2.0 * nnz_total / (e2e_ms * 1e-3) / 1e9, 3),
+                        "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": int(tsum[1]),
+                        "d2h_bytes_per_step": int(tsum[2]),
+                        "path": e2e["path"] + f"; {world} ranks, max over ranks"})
+        line["e2e"] = e2e
+        if world == 1:
+            line["e2e_cold"] = e2e_host(A, args, lib, dev, nnz_total)
     if not args.no_cpu_baseline and rank == 0 and world == 1:
         line["cpu_baseline"] = cpu_baseline(A, args)
     if rank == 0:
