@@ -237,10 +237,17 @@ def power_arm(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # LW_BENCH_SHARE_GPU=1 (code-path check only, never a measurement): every
+    # rank on cuda:0 over gloo, so the N > 1 path runs on a one-GPU box
+    share = os.environ.get("LW_BENCH_SHARE_GPU") == "1"
+    local = 0 if share else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     dtype = "float32" if args.dtype == "fp32" else "float64"
     full = lwb.generate_rmat_csr(args.scale, args.edge_factor, args.seed, dtype=dtype, device=dev)
     n, nnz_total = full.rows, full.nnz
@@ -352,10 +359,17 @@ def our_arm(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # LW_BENCH_SHARE_GPU=1 (code-path check only, never a measurement): every
+    # rank on cuda:0 over gloo, so the N > 1 path runs on a one-GPU box
+    share = os.environ.get("LW_BENCH_SHARE_GPU") == "1"
+    local = 0 if share else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
         if world > 1:
