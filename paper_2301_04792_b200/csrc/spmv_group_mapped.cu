@@ -89,8 +89,11 @@ __device__ __forceinline__ void gather_loaded(const StepLoads<ValT, U>& L, const
 }
 
 // ---- warp tiles -------------------------------------------------------------------
+#ifndef LW_GW_MINB
+#define LW_GW_MINB 0
+#endif
 template <class OffT, class ValT, bool PROBE>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, LW_GW_MINB)
     k_group_warp(Csr<OffT, ValT> A, const ValT* __restrict__ x, ValT* __restrict__ y,
                  int64_t groups, Probe probe) {
     __shared__ double s_acc[8][kWarp];
@@ -318,10 +321,40 @@ static GroupKernel pick_group_kernel(int64_t lanes, int64_t gs, int64_t tpb) {
     return GK_GENERIC;
 }
 
+// Groups one SM holds at once for the warp / block kernels (their register use,
+// not 2048 threads, sets it), so the auto lane count is one full wave.
+template <class K>
+static int64_t resident_ctas(K kern, int nt) {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, nt, 0) != cudaSuccess || n < 1) return 0;
+    return n;
+}
+static int64_t groups_per_sm(int64_t gs, int64_t tpb) {
+#ifndef LW_GROUP_OCC
+#define LW_GROUP_OCC 1
+#endif
+    if (LW_GROUP_OCC) {
+        if (gs == 32 && tpb == 32) {
+            static const int64_t w = resident_ctas(k_group_warp<int32_t, float, false>, 256) * 8;
+            if (w > 0) return w;
+        } else if (gs == tpb && gs == 256) {
+            static const int64_t b = resident_ctas(k_group_block<int32_t, float, 256, false>, 256);
+            if (b > 0) return b;
+        } else if (gs == tpb && gs == 128) {
+            static const int64_t b = resident_ctas(k_group_block<int32_t, float, 128, false>, 128);
+            if (b > 0) return b;
+        } else if (gs == tpb && gs == 64) {
+            static const int64_t b = resident_ctas(k_group_block<int32_t, float, 64, false>, 64);
+            if (b > 0) return b;
+        }
+    }
+    return gs < 2048 ? 2048 / gs : 1;
+}
+
 int64_t group_auto_lanes(int64_t rows, int64_t gs, int64_t tpb) {
     const int64_t nblocks = rows > 0 ? ceil_div(rows, tpb) : 1;
-    // enough groups to fill every SM at full occupancy, but never more than blocks
-    const int64_t per_sm = gs < 2048 ? 2048 / gs : 1;
+    // enough groups to fill every SM once, but never more than blocks
+    const int64_t per_sm = groups_per_sm(gs, tpb);
     const int64_t cap = (int64_t)sm_count() * per_sm;
     const int64_t groups = nblocks < cap ? nblocks : cap;
     return (groups > 0 ? groups : 1) * gs;

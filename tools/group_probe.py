@@ -1,7 +1,8 @@
 import os, sys, torch
 sys.path.insert(0, '.')
 import paper_2301_04792_b200 as lw
-mats = [("pl1M", lw.generate_power_law_csr(1_000_000, 16.0, 1.1, seed=1).to_device("float32")),
+mats = [("C2b", lw.generate_banded_device(1_000_000, 16, seed=1)),
+        ("pl1M", lw.generate_power_law_csr(1_000_000, 16.0, 1.1, seed=1).to_device("float32")),
         ("C2u", lw.generate_random_csr(1_000_000, 1_000_000, 32_000_000, seed=2).to_device("float32")),
         ("C3", lw.generate_rmat_csr(24, 16, seed=3))]
 for name, A in mats:
