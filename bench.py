@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--seed", type=int, default=3)
     ap.add_argument("--dtype", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--cpu-reps", type=int, default=3)
+    ap.add_argument("--hot-x", default="auto", choices=["auto", "on", "off"],
+                    help="work_oriented: hot-x column packing (DESIGN.md 4e); auto = fp32 only")
+    ap.add_argument("--max-hot", type=int, default=0, help="hot-x slots (0 = library default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--mode", default="spmv", choices=["spmv", "power"],
@@ -82,7 +85,7 @@ def ncu_traffic(workload: str, dtype: str, schedule: str):
     """DRAM bytes per launch of the dominant kernel from the newest committed
     ncu --set full capture (profiles/*/ncu_traffic.json) for this workload."""
     best = None
-    for f in sorted((ROOT / "profiles").glob("*/ncu_traffic.json")):
+    for f in sorted((ROOT / "profiles").glob("*/ncu_traffic*.json")):
         try:
             d = json.loads(f.read_text())
         except Exception:
@@ -410,24 +413,44 @@ def our_arm(args):
         ws_bytes = lib.lw_spmv_workspace(_lib.LW_MERGE_PATH, A.rows, A.nnz, lanes, Ac.dtype)
         ws = torch.empty(max(ws_bytes, 256), dtype=torch.uint8, device=dev)
 
+    # hot-x column packing (one-time inspector, outside the timed region like the
+    # matrix upload): fp32 work_oriented by default, measured slower for fp64
+    hx, hx_build_ms = None, None
+    if sched is lwb.ScheduleKind.MERGE_PATH and (args.hot_x == "on" or
+                                                 (args.hot_x == "auto" and args.dtype == "fp32")):
+        torch.cuda.synchronize()
+        t_b = time.perf_counter()
+        hx = A.pack_hot_columns(args.max_hot or None)
+        torch.cuda.synchronize()
+        hx_build_ms = (time.perf_counter() - t_b) * 1e3
+        hx_ws_bytes = lib.lw_spmv_work_oriented_hotx_workspace(A.rows, A.nnz, lanes, hx.n_hot, Ac.dtype)
+        hx_ws = torch.empty(max(hx_ws_bytes, 256), dtype=torch.uint8, device=dev)
+        Hc = hx.packed.c_struct()
+        hot_ptr = hx.hot_cols.data_ptr() if hx.n_hot else None
+
     # one step, with the dominant kernel bracketed by events
     ev = []
 
-    def step(record):
+    def phase(mask, packed):
+        if packed:
+            return lib.lw_spmv_work_oriented_hotx_phases(Hc, hot_ptr, hx.n_hot, x.data_ptr(), y.data_ptr(),
+                                                         lanes, hx_ws.data_ptr(), hx_ws.numel(), mask, sp)
+        return lib.lw_spmv_work_oriented_phases(Ac, x.data_ptr(), y.data_ptr(), lanes, ws.data_ptr(),
+                                                ws.numel(), mask, sp)
+
+    def step(record, packed=None):
+        packed = hx is not None if packed is None else packed
         if sched is lwb.ScheduleKind.MERGE_PATH:
-            _lib.check(lib.lw_spmv_work_oriented_phases(Ac, x.data_ptr(), y.data_ptr(), lanes,
-                                                        ws.data_ptr(), ws.numel(), 1, sp), "p1")
+            _lib.check(phase(1, packed), "p1")
             if record:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-            _lib.check(lib.lw_spmv_work_oriented_phases(Ac, x.data_ptr(), y.data_ptr(), lanes,
-                                                        ws.data_ptr(), ws.numel(), 2, sp), "p2")
+            _lib.check(phase(2, packed), "p2")
             if record:
                 e1 = torch.cuda.Event(enable_timing=True)
                 e1.record(stream)
                 ev.append((e0, e1))
-            _lib.check(lib.lw_spmv_work_oriented_phases(Ac, x.data_ptr(), y.data_ptr(), lanes,
-                                                        ws.data_ptr(), ws.numel(), 4, sp), "p3")
+            _lib.check(phase(4, packed), "p3")
         else:
             if record:
                 e0 = torch.cuda.Event(enable_timing=True)
@@ -460,6 +483,26 @@ def our_arm(args):
         step(True)
     torch.cuda.synchronize()
     kern_ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    if hx is not None:
+        y_packed = y.clone()
+        # pass C: the unpacked kernel on the same inputs (bit-identical y), for the record
+        for _ in range(3):
+            step(False, packed=False)
+        torch.cuda.synchronize()
+        u0 = torch.cuda.Event(enable_timing=True)
+        u1 = torch.cuda.Event(enable_timing=True)
+        u0.record(stream)
+        for _ in range(args.steps):
+            step(False, packed=False)
+        u1.record(stream)
+        torch.cuda.synchronize()
+        ms_unpacked = u0.elapsed_time(u1) / args.steps
+        ev.clear()
+        for _ in range(args.steps):
+            step(True, packed=False)
+        torch.cuda.synchronize()
+        kern_unpacked = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+        same = bool(torch.equal(y, y_packed))
 
     ms = ms_total / args.steps
     if world > 1:
@@ -475,7 +518,8 @@ def our_arm(args):
     hbm, hbm_src = peaks()
     achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
     workload = f"rmat{args.scale}-ef{args.edge_factor}-seed{args.seed}"
-    tr = ncu_traffic(workload, "f32" if args.dtype == "fp32" else "f64", args.schedule) if world == 1 else None
+    tr_key = args.schedule + ("+hotx" if hx is not None else "")
+    tr = ncu_traffic(workload, "f32" if args.dtype == "fp32" else "f64", tr_key) if world == 1 else None
     traffic = tr[0] if tr else None
     line = {
         "metric": METRIC, "value": round(gflops, 3), "unit": "GFLOP/s", "n_gpus": world,
@@ -496,9 +540,18 @@ def our_arm(args):
                      "achieved_gather_every_nnz": round(gather_bytes / (kern_ms * 1e-3) / 1e9, 1),
                      "frac_gather_every_nnz": round(gather_bytes / (kern_ms * 1e-3) / 1e9 / hbm, 4)},
         "hbm_gbs_step": round(alg_bytes / (ms * 1e-3) / 1e9, 1),
-        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches": (launches_per_step + (hx is not None)) * args.steps,
         "clocks": clocks.summary(),
     }
+    if hx is not None:
+        line["config"]["x_layout"] = (f"hot-x packed: {hx.n_hot} most gathered columns in a dense "
+                                      f"per-call copy kept in L1 (DESIGN.md 4e); one-time inspector "
+                                      f"{hx_build_ms:.1f} ms outside the timed region")
+        line["roofline"]["kernel"] = "k_hot_pack + k_wo_chunk"
+        line["unpacked"] = {"ms_per_step": round(ms_unpacked, 4), "kernel_ms": round(kern_unpacked, 4),
+                            "value": round(2.0 * nnz_total / (ms_unpacked * 1e-3) / 1e9, 3),
+                            "frac": round(alg_bytes / (kern_unpacked * 1e-3) / 1e9 / hbm, 4),
+                            "y_bit_identical": same}
 
     # e2e through the C ABI with HOST x and y (pinned), copies inside the timed
     # region; the matrix is the resident operator (uploaded once, like weights).
@@ -547,7 +600,13 @@ def e2e_resident(A, args, lib, dev, nnz_total):
     d_y = [torch.empty(A.rows, dtype=A.dtype, device=dev) for _ in range(2)]
     Ac = A.c_struct()
     s_in, s_comp, s_out = (torch.cuda.Stream(dev) for _ in range(3))
-    ws_b = lib.lw_spmv_workspace(_lib.LW_MERGE_PATH, A.rows, A.nnz, 0, Ac.dtype)
+    hx = A.hot_columns()   # the packed operator when the bench built one (hot-x)
+    if hx is not None:
+        Hc = hx.packed.c_struct()
+        hot_ptr = hx.hot_cols.data_ptr() if hx.n_hot else None
+        ws_b = lib.lw_spmv_work_oriented_hotx_workspace(A.rows, A.nnz, 0, hx.n_hot, Ac.dtype)
+    else:
+        ws_b = lib.lw_spmv_workspace(_lib.LW_MERGE_PATH, A.rows, A.nnz, 0, Ac.dtype)
     ws = torch.empty(max(ws_b, 256), dtype=torch.uint8, device=dev)
     ev_x = [torch.cuda.Event() for _ in range(2)]
     ev_c = [torch.cuda.Event() for _ in range(2)]
@@ -563,8 +622,13 @@ def e2e_resident(A, args, lib, dev, nnz_total):
             ev_x[b].record(s_in)
         s_comp.wait_event(ev_x[b])
         s_comp.wait_event(ev_o[b])              # y buffer b free (download i-2 done)
-        _lib.check(lib.lw_spmv(_lib.LW_MERGE_PATH, Ac, d_x[b].data_ptr(), d_y[b].data_ptr(), 0, 32,
-                               32, ws.data_ptr(), ws.numel(), int(s_comp.cuda_stream)), "lw_spmv")
+        if hx is not None:
+            _lib.check(lib.lw_spmv_work_oriented_hotx(Hc, hot_ptr, hx.n_hot, d_x[b].data_ptr(),
+                                                      d_y[b].data_ptr(), 0, ws.data_ptr(), ws.numel(),
+                                                      int(s_comp.cuda_stream)), "lw_spmv_work_oriented_hotx")
+        else:
+            _lib.check(lib.lw_spmv(_lib.LW_MERGE_PATH, Ac, d_x[b].data_ptr(), d_y[b].data_ptr(), 0, 32,
+                                   32, ws.data_ptr(), ws.numel(), int(s_comp.cuda_stream)), "lw_spmv")
         ev_c[b].record(s_comp)
         with torch.cuda.stream(s_out):
             s_out.wait_event(ev_c[b])
@@ -590,7 +654,8 @@ def e2e_resident(A, args, lib, dev, nnz_total):
             "h2d_bytes_per_step": int(h_x[0].numel() * h_x[0].element_size()),
             "d2h_bytes_per_step": int(h_y[0].numel() * h_y[0].element_size()),
             "ms_per_step": round(ms, 3), "steps": steps,
-            "path": ("lw_spmv (C ABI) per step; pinned host x copied in and y copied out every "
+            "path": (("lw_spmv_work_oriented_hotx" if hx is not None else "lw_spmv") +
+                     " (C ABI) per step; pinned host x copied in and y copied out every "
                      "step on separate streams, double-buffered so uploads/downloads overlap "
                      "the neighbouring steps' SpMV; matrix resident in HBM (uploaded once, "
                      "outside the timed region)")}

@@ -137,6 +137,32 @@ int lw_spmv_work_oriented_phases(const lw_csr_t* A, const void* x, void* y, int6
                                  void* workspace, size_t workspace_bytes,
                                  uint32_t phase_mask, uintptr_t stream);
 
+/* Hot-x column packing: an inspector-executor form of the
+ * work_oriented SpMV for power-law matrices. No reference counterpart — it is a
+ * B200 layout step in front of lw_spmv_work_oriented; y is bit-identical.
+ * lw_hotx_build (one-time, per matrix; synchronizes `stream`, reads two 256 KB
+ * histograms on the host): picks the hot set H = {c : count(c) >= T}, T the
+ * smallest threshold >= 2 with |H| <= max_hot (<= 32768), writes hot_cols[|H|]
+ * (ascending) and col_packed[nnz] (hot columns -> slot | 0x80000000), *n_hot_out
+ * = |H|. lw_spmv_work_oriented_hotx: A's col_indices must be col_packed; packs
+ * xh[s] = x[hot_cols[s]] into the workspace, then runs the work_oriented SpMV
+ * with hot gathers kept in L1 and cold ones bypassing it. */
+size_t lw_hotx_build_workspace(int64_t cols);
+int lw_hotx_build(const lw_csr_t* A, int32_t max_hot, int32_t* col_packed, int32_t* hot_cols,
+                  int32_t* n_hot_out, void* workspace, size_t workspace_bytes, uintptr_t stream);
+size_t lw_spmv_work_oriented_hotx_workspace(int64_t rows, int64_t nnz, int64_t lanes,
+                                            int32_t n_hot, int32_t dtype);
+int lw_spmv_work_oriented_hotx(const lw_csr_t* A_packed, const int32_t* hot_cols, int32_t n_hot,
+                               const void* x, void* y, int64_t lanes, void* workspace,
+                               size_t workspace_bytes, uintptr_t stream);
+
+/* The same in three stream-ordered phases (bit 0 partition, bit 1 pack + SpMV
+ * chunk kernel, bit 2 carry fix-up), as lw_spmv_work_oriented_phases. */
+int lw_spmv_work_oriented_hotx_phases(const lw_csr_t* A_packed, const int32_t* hot_cols,
+                                      int32_t n_hot, const void* x, void* y, int64_t lanes,
+                                      void* workspace, size_t workspace_bytes,
+                                      uint32_t phase_mask, uintptr_t stream);
+
 /* work_oriented SpMV fused with the all-gather of the power iteration (BASELINE
  * C5): every row this rank's shard produces is written to y AND to
  * element row_base + row of each rank's next-x buffer -- through the NVLS

@@ -11,7 +11,7 @@ kernels (liblwb200.so, C ABI in include/lw_b200.h); there is no CPU fallback.
 from ._backend import (ENV_VAR, NUMBA_AVAILABLE, backend_name, cuda_active, cuda_available,
                        numba_active, use_backend)
 from ._lib import BackendUnavailable
-from .device import (DeviceCsr, device_group_plan_prefix, device_merge_path_partition,
+from .device import (DeviceCsr, HotColumns, device_group_plan_prefix, device_merge_path_partition,
                      generate_banded_device, generate_rmat_csr)
 from .executor import (SENTINEL_TILE, SUM_CARRIES, AtomicMinArray, CarryOut, CarryPolicy,
                        ExecutorConfig, ImbalanceReport, atomic_min_real, device_config,
@@ -36,6 +36,7 @@ from .work import (TileSet, csr_tile_set, infinite_range, lane_stride_range, ste
 __version__ = "0.1.0"
 
 __all__ = [
+    "HotColumns",
     "AtomicMinArray", "SsspState", "UNREACHED", "atomic_min_real", "bfs", "bfs_pass",
     "device_graph", "sssp", "sssp_init", "sssp_pass",
     "BackendUnavailable", "NUMBA_AVAILABLE", "CarryOut", "CarryPolicy", "CooMatrix", "CsrMatrix", "Graph",

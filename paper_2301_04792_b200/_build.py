@@ -27,6 +27,7 @@ SOURCES = [
     "lw_abi.cu",
     "spmv_thread_mapped.cu",
     "spmv_work_oriented.cu",
+    "hotx.cu",
     "spmv_group_mapped.cu",
     "spmm.cu",
     "frontier.cu",

@@ -41,6 +41,11 @@ EXPORTS = (
     "lw_spmv_work_oriented",
     "lw_spmv_work_oriented_phases",
     "lw_spmv_work_oriented_peers",
+    "lw_hotx_build_workspace",
+    "lw_hotx_build",
+    "lw_spmv_work_oriented_hotx_workspace",
+    "lw_spmv_work_oriented_hotx",
+    "lw_spmv_work_oriented_hotx_phases",
     "lw_norm_workspace",
     "lw_vector_norm",
     "lw_vector_scale",
@@ -132,6 +137,12 @@ _SIGNATURES = {
     "lw_spmv_work_oriented_phases": (ctypes.c_int, [_csr_p, _vp, _vp, _i64, _vp, _sz, _u32, _up]),
     "lw_spmv_work_oriented_peers": (ctypes.c_int, [_csr_p, _vp, _vp, _i64, _vp, _sz, _i32, _vp, _u64,
                                                    _i64, _up]),
+    "lw_hotx_build_workspace": (_sz, [_i64]),
+    "lw_hotx_build": (ctypes.c_int, [_csr_p, _i32, _vp, _vp, ctypes.POINTER(_i32), _vp, _sz, _up]),
+    "lw_spmv_work_oriented_hotx_workspace": (_sz, [_i64, _i64, _i64, _i32, _i32]),
+    "lw_spmv_work_oriented_hotx": (ctypes.c_int, [_csr_p, _vp, _i32, _vp, _vp, _i64, _vp, _sz, _up]),
+    "lw_spmv_work_oriented_hotx_phases": (ctypes.c_int, [_csr_p, _vp, _i32, _vp, _vp, _i64, _vp, _sz,
+                                                         _u32, _up]),
     "lw_norm_workspace": (_sz, [_i64]),
     "lw_vector_norm": (ctypes.c_int, [_vp, _i64, _i32, _vp, _sz, _vp, _up]),
     "lw_vector_scale": (ctypes.c_int, [_vp, _i64, _i32, _vp, _vp, _up]),
@@ -184,7 +195,10 @@ def load(path: Path | str | None = None):
         except OSError as exc:  # pragma: no cover - depends on the box
             _load_error = f"cannot load {p}: {exc}"
             raise BackendUnavailable(_load_error) from exc
+        variant = "LWB200_LIB" in os.environ and not path   # A/B builds may predate new entries
         for name, (res, args) in _SIGNATURES.items():
+            if variant and not hasattr(lib, name):
+                continue
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

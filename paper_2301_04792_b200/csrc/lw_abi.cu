@@ -26,6 +26,11 @@ int vector_norm(const void*, int64_t, int, void*, double*, cudaStream_t);
 int vector_scale(const void*, int64_t, int, const double*, void*, cudaStream_t);
 int spmv_work_oriented_peers(const lw_csr_t*, const void*, void*, int64_t, void*, size_t, int32_t,
                              const uint64_t*, uint64_t, int64_t, cudaStream_t);
+size_t wo_hotx_workspace(int64_t rows, int64_t nnz, int64_t lanes, int64_t n_hot, int dtype);
+int spmv_work_oriented_hotx(const lw_csr_t*, const int32_t*, int32_t, const void*, void*, int64_t, void*,
+                            size_t, unsigned, cudaStream_t);
+size_t hotx_build_workspace(int64_t cols);
+int hotx_build(const lw_csr_t*, int32_t, int32_t*, int32_t*, int32_t*, void*, size_t, cudaStream_t);
 int frontier_compact(const uint8_t*, int64_t, int32_t*, int64_t*, void*, cudaStream_t);
 int sssp_pass(const lw_csr_t*, const int32_t*, int64_t, double*, uint8_t*, int, int64_t, int64_t, int64_t, void*, cudaStream_t);
 int bfs_pass(const lw_csr_t*, const int32_t*, int64_t, int64_t*, int64_t, uint8_t*, int, int64_t, int64_t, int64_t, void*, cudaStream_t);
@@ -177,6 +182,44 @@ int lw_spmv_work_oriented_peers(const lw_csr_t* A, const void* x, void* y, int64
     if (lanes < 0 || (n_peers == 0 && multicast_ptr == 0)) return LW_E_INVALID_ARG;
     return spmv_work_oriented_peers(A, x, y, lanes, ws, ws_bytes, n_peers, peer_ptrs, multicast_ptr,
                                     row_base, (cudaStream_t)stream);
+}
+
+size_t lw_hotx_build_workspace(int64_t cols) { return cols < 0 ? 0 : hotx_build_workspace(cols); }
+
+int lw_hotx_build(const lw_csr_t* A, int32_t max_hot, int32_t* col_packed, int32_t* hot_cols,
+                  int32_t* n_hot_out, void* ws, size_t ws_bytes, uintptr_t stream) {
+    int rc = check_csr(A);
+    if (rc) return rc;
+    return hotx_build(A, max_hot, col_packed, hot_cols, n_hot_out, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+size_t lw_spmv_work_oriented_hotx_workspace(int64_t rows, int64_t nnz, int64_t lanes, int32_t n_hot,
+                                            int32_t dtype) {
+    if (rows < 0 || nnz < 0 || lanes < 0 || n_hot < 0) return 0;
+    return wo_hotx_workspace(rows, nnz, lanes, n_hot, dtype);
+}
+
+int lw_spmv_work_oriented_hotx(const lw_csr_t* A, const int32_t* hot_cols, int32_t n_hot,
+                               const void* x, void* y, int64_t lanes, void* ws, size_t ws_bytes,
+                               uintptr_t stream) {
+    int rc = check_csr(A);
+    if (rc) return rc;
+    if (A->rows > 0 && !y) return LW_E_INVALID_ARG;
+    if (A->nnz > 0 && !x) return LW_E_INVALID_ARG;
+    if (lanes < 0) return LW_E_INVALID_ARG;
+    return spmv_work_oriented_hotx(A, hot_cols, n_hot, x, y, lanes, ws, ws_bytes, 7u, (cudaStream_t)stream);
+}
+
+int lw_spmv_work_oriented_hotx_phases(const lw_csr_t* A, const int32_t* hot_cols, int32_t n_hot,
+                                      const void* x, void* y, int64_t lanes, void* ws,
+                                      size_t ws_bytes, uint32_t phase_mask, uintptr_t stream) {
+    int rc = check_csr(A);
+    if (rc) return rc;
+    if (A->rows > 0 && !y) return LW_E_INVALID_ARG;
+    if (A->nnz > 0 && !x) return LW_E_INVALID_ARG;
+    if (lanes < 0 || phase_mask == 0 || phase_mask > 7u) return LW_E_INVALID_ARG;
+    return spmv_work_oriented_hotx(A, hot_cols, n_hot, x, y, lanes, ws, ws_bytes, phase_mask,
+                                   (cudaStream_t)stream);
 }
 
 int lw_spmv_group_mapped(const lw_csr_t* A, const void* x, void* y, int64_t lanes,

@@ -34,6 +34,9 @@ namespace lw {
 #endif
 constexpr int WO_W = LW_WO_W;
 constexpr int WO_S = WO_W - 16;
+#ifndef LW_WO_BATCH   // A/B: batch the unpacked kernel's gathers like the packed one's
+#define LW_WO_BATCH 0
+#endif
 constexpr unsigned WO_PHASE_PARTITION = 1, WO_PHASE_SPMV = 2, WO_PHASE_FIXUP = 4;
 
 // threads x atoms-per-thread covering the window: one 32-byte col_idx load and
@@ -229,12 +232,36 @@ __device__ __forceinline__ void store_run(double* dst, const double* v) {
     for (int h = 0; h < IPT / 2; ++h) d[h] = make_double2(v[2 * h], v[2 * h + 1]);
 }
 
-template <class OffT, class ValT, bool PROBE, bool VEC, bool PEERS = false>
+// Hot-x packed gather (lw_hotx_build relabels the most gathered columns c to
+// slot | 0x80000000 and lw_spmv_work_oriented_hotx packs xh[slot] = x[c] per
+// call): the packed hot values, 8 per 32-byte sector, are kept in L1
+// (evict_last) and every other gather bypasses L1 (no_allocate), so the cold
+// misses cannot evict the hot lines. Both loads stay on the read-only path.
+__device__ __forceinline__ float ld_hotx(const float* x, const float* xh, int32_t c) {
+    float v;
+    if (c < 0)
+        LW_LDASM("ld.global.nc.L1::evict_last.f32 %0, [%1];" : "=f"(v) : "l"(xh + (c & 0x7fffffff)));
+    else
+        LW_LDASM("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;"
+                 : "=f"(v) : "l"(x + c), "l"(policy_evict_last()));
+    return v;
+}
+__device__ __forceinline__ double ld_hotx(const double* x, const double* xh, int32_t c) {
+    double v;
+    if (c < 0)
+        LW_LDASM("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(xh + (c & 0x7fffffff)));
+    else
+        LW_LDASM("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+                 : "=d"(v) : "l"(x + c), "l"(policy_evict_last()));
+    return v;
+}
+
+template <class OffT, class ValT, bool PROBE, bool VEC, bool PEERS = false, bool HOT = false>
 __global__ void __launch_bounds__(WoCfg<ValT>::NT)
     k_wo_chunk(Csr<OffT, ValT> A, const ValT* __restrict__ x, ValT* __restrict__ y,
                int64_t items, int64_t J, const int64_t* __restrict__ bound_tile,
                int64_t* __restrict__ carry_tile, double* __restrict__ carry_val, Probe probe,
-               PeerOut po = PeerOut{}) {
+               PeerOut po = PeerOut{}, const ValT* __restrict__ xh = nullptr) {
     constexpr int NT = WoCfg<ValT>::NT, IPT = WoCfg<ValT>::IPT;
     constexpr int W = WO_W, S = WO_S;
     static_assert(NT * IPT == W, "window must be NT*IPT atoms");
@@ -280,7 +307,13 @@ __global__ void __launch_bounds__(WoCfg<ValT>::NT)
             int32_t c[IPT];
             ValT v[IPT];
 #pragma unroll
-            for (int k = 0; k < IPT; ++k) { c[k] = 0; v[k] = (ValT)0; }
+            for (int k = 0; k < IPT; ++k) {
+                // atoms past the window still issue their (discarded) gather: point it at
+                // x[0] (L1-allocating) or, packed, at hot slot 0 (kept in L1), never at a
+                // no_allocate load that would cost an L2 request
+                c[k] = HOT ? (int32_t)0x80000000 : 0;
+                v[k] = (ValT)0;
+            }
             if (pos < w1) {
                 if (VEC && g + IPT <= A.nnz) {
                     ld_atoms<IPT>(A.col + g, A.val + g, c, v);
@@ -291,10 +324,20 @@ __global__ void __launch_bounds__(WoCfg<ValT>::NT)
                 }
             }
             if (row0) e0 = (int32_t)(ld_off(A.off + t0 + 1 + tid) - base);
+            if constexpr (HOT || LW_WO_BATCH) {
+                // all IPT gathers issued back to back, unconditionally (every c[k] is
+                // a valid column, x[0] or hot slot 0), before the first product consumes one
+#pragma unroll
+                for (int k = 0; k < IPT; ++k) {
+                    if constexpr (HOT) p[k] = ld_hotx(x, xh, c[k]);
+                    else p[k] = ld_gather(x + c[k]);
+                }
+            }
 #pragma unroll
             for (int k = 0; k < IPT; ++k) {
                 const bool in = pos + k >= w0 && pos + k < w1;
-                p[k] = in ? v[k] * ld_gather(x + c[k]) : (ValT)0;
+                if constexpr (HOT || LW_WO_BATCH) p[k] = in ? v[k] * p[k] : (ValT)0;
+                else p[k] = in ? v[k] * ld_gather(x + c[k]) : (ValT)0;
             }
         }
 
@@ -429,6 +472,14 @@ __global__ void k_carry_fixup(const int64_t* __restrict__ carry_tile,
     if (PEERS) peer_store(po, r, v);
 }
 
+// ---- 4. hot-x pack: xh[slot] = x[hot_cols[slot]] (n_hot gathers per call) ----------------
+template <class ValT>
+__global__ void k_hot_pack(const ValT* __restrict__ x, const int32_t* __restrict__ hot_cols,
+                           int32_t n_hot, ValT* __restrict__ xh) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n_hot) xh[i] = x[hot_cols[i]];
+}
+
 // ---- host side -------------------------------------------------------------------
 struct WoPlan {
     int64_t total, lanes, items, J;
@@ -495,11 +546,11 @@ int merge_path_partition(int64_t rows, int64_t nnz, const void* off, int bits, i
                                   coords, s);
 }
 
-template <class OffT, class ValT, bool PR, bool VEC>
+template <class OffT, class ValT, bool PR, bool VEC, bool HOT = false>
 static int launch_chunk(const Csr<OffT, ValT>& a, const ValT* x, ValT* y, const WoPlan& p,
                         const int64_t* tiles, int64_t* c_tile, double* c_val, const Probe& pr,
-                        cudaStream_t s) {
-    auto kern = k_wo_chunk<OffT, ValT, PR, VEC>;
+                        cudaStream_t s, const ValT* xh = nullptr) {
+    auto kern = k_wo_chunk<OffT, ValT, PR, VEC, false, HOT>;
     constexpr size_t smem = WoSmem<ValT>::bytes;
     static bool attr = false;   // one-time opt-in above the 48 KB default
     if (!attr) {
@@ -509,14 +560,15 @@ static int launch_chunk(const Csr<OffT, ValT>& a, const ValT* x, ValT* y, const 
         attr = true;
     }
     kern<<<(unsigned)p.lanes, WoCfg<ValT>::NT, smem, s>>>(a, x, y, p.items, p.J, tiles, c_tile,
-                                                         c_val, pr, PeerOut{});
+                                                         c_val, pr, PeerOut{}, xh);
     LW_LAUNCH_CHECK();
     return LW_OK;
 }
 
 template <class OffT, class ValT>
 static int launch_wo(const lw_csr_t* A, const void* x, void* y, const WoPlan& p, void* ws,
-                     const lw_probe_t* probe, unsigned phases, cudaStream_t s) {
+                     const lw_probe_t* probe, unsigned phases, cudaStream_t s,
+                     const int32_t* hot_cols = nullptr, int32_t n_hot = 0) {
     Csr<OffT, ValT> a{A->rows, A->cols, A->nnz, (const OffT*)A->row_offsets,
                       A->col_indices, (const ValT*)A->values};
     const size_t nb = (size_t)(p.lanes * p.J + 1), nc = wo_carries(p);
@@ -542,7 +594,15 @@ static int launch_wo(const lw_csr_t* A, const void* x, void* y, const WoPlan& p,
         ValT* yv = (ValT*)y;
         const bool P = probe != nullptr;
         int rc = LW_OK;
-        if (P) rc = vec ? launch_chunk<OffT, ValT, true, true>(a, xv, yv, p, tiles, c_tile, c_val, pr, s)
+        if (hot_cols) {   // packed hot x lives after the carries in the workspace
+            ValT* xh = (ValT*)(w + align_up(nb * 8, 256) + 2 * align_up(nc * 8, 256));
+            if (n_hot > 0) {
+                k_hot_pack<ValT><<<(unsigned)ceil_div(n_hot, 256), 256, 0, s>>>(xv, hot_cols, n_hot, xh);
+                LW_LAUNCH_CHECK();
+            }
+            rc = vec ? launch_chunk<OffT, ValT, false, true, true>(a, xv, yv, p, tiles, c_tile, c_val, pr, s, xh)
+                     : launch_chunk<OffT, ValT, false, false, true>(a, xv, yv, p, tiles, c_tile, c_val, pr, s, xh);
+        } else if (P) rc = vec ? launch_chunk<OffT, ValT, true, true>(a, xv, yv, p, tiles, c_tile, c_val, pr, s)
                         : launch_chunk<OffT, ValT, true, false>(a, xv, yv, p, tiles, c_tile, c_val, pr, s);
         else   rc = vec ? launch_chunk<OffT, ValT, false, true>(a, xv, yv, p, tiles, c_tile, c_val, pr, s)
                         : launch_chunk<OffT, ValT, false, false>(a, xv, yv, p, tiles, c_tile, c_val, pr, s);
@@ -579,7 +639,7 @@ static int launch_wo_peers(const lw_csr_t* A, const void* x, void* y, const WoPl
         attr[vec] = true;
     }
     kern<<<(unsigned)p.lanes, WoCfg<ValT>::NT, smem, s>>>(a, (const ValT*)x, (ValT*)y, p.items, p.J,
-                                                         tiles, c_tile, c_val, Probe{}, po);
+                                                         tiles, c_tile, c_val, Probe{}, po, nullptr);
     LW_LAUNCH_CHECK();
     k_carry_fixup<ValT, true><<<ceil_div(p.lanes, 256), 256, 0, s>>>(c_tile, c_val, p.lanes, (ValT*)y,
                                                                      a.rows, po);
@@ -620,6 +680,29 @@ int spmv_work_oriented(const lw_csr_t* A, const void* x, void* y, int64_t lanes,
                    : launch_wo<int64_t, float>(A, x, y, p, ws, probe, phases, s);
     return o32 ? launch_wo<int32_t, double>(A, x, y, p, ws, probe, phases, s)
                : launch_wo<int64_t, double>(A, x, y, p, ws, probe, phases, s);
+}
+
+// Workspace of the hot-x variant: the plain one plus the packed hot values.
+size_t wo_hotx_workspace(int64_t rows, int64_t nnz, int64_t lanes, int64_t n_hot, int dtype) {
+    // at least one slot: atoms outside a chunk's window read (and discard) slot 0
+    return wo_workspace(rows, nnz, lanes) + align_up((size_t)(n_hot > 0 ? n_hot : 1) * (dtype == LW_F32 ? 4 : 8), 256);
+}
+
+int spmv_work_oriented_hotx(const lw_csr_t* A, const int32_t* hot_cols, int32_t n_hot,
+                            const void* x, void* y, int64_t lanes, void* ws, size_t ws_bytes,
+                            unsigned phases, cudaStream_t s) {
+    if (n_hot < 0 || (n_hot > 0 && !hot_cols)) return LW_E_INVALID_ARG;
+    const WoPlan p = wo_plan(A->rows, A->nnz, lanes);
+    if (A->rows == 0) return LW_OK;
+    if (!ws || ws_bytes < wo_hotx_workspace(A->rows, A->nnz, lanes, n_hot, A->dtype)) return LW_E_WORKSPACE;
+    static const int32_t none = 0;   // any non-null marker selects the hot kernel when n_hot == 0
+    const int32_t* hc = hot_cols ? hot_cols : &none;
+    const bool o32 = A->offset_bits == 32;
+    if (A->dtype == LW_F32)
+        return o32 ? launch_wo<int32_t, float>(A, x, y, p, ws, nullptr, phases, s, hc, n_hot)
+                   : launch_wo<int64_t, float>(A, x, y, p, ws, nullptr, phases, s, hc, n_hot);
+    return o32 ? launch_wo<int32_t, double>(A, x, y, p, ws, nullptr, phases, s, hc, n_hot)
+               : launch_wo<int64_t, double>(A, x, y, p, ws, nullptr, phases, s, hc, n_hot);
 }
 
 }  // namespace lw

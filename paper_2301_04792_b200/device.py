@@ -158,6 +158,48 @@ class DeviceCsr:
         s.dtype = _dtype_code(self.dtype)
         return s
 
+    # ---- hot-x column packing (csrc/hotx.cu) ----------------------
+    def pack_hot_columns(self, max_hot: int | None = None) -> "HotColumns":
+        """Build (once) the hot-x packing the work_oriented SpMV then uses.
+
+        The at most ``max_hot`` most gathered columns (default 48 KB of values:
+        12288 fp32 / 6144 fp64) get dense slots of a per-call packed x that the
+        kernel keeps in L1; y stays bit-identical to the unpacked kernel. Costs
+        one int32 copy of col_indices. Synchronizes the current stream once.
+        """
+        torch = _torch()
+        if max_hot is None:
+            max_hot = 49152 // self.values.element_size()
+        max_hot = int(max_hot)
+        hit = self.hot_columns()
+        if hit is not None and hit.max_hot == max_hot:
+            return hit
+        lib = _lib.load()
+        A = self.c_struct()
+        col_packed = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=self.device)
+        hot = torch.empty(max(max_hot, 1), dtype=torch.int32, device=self.device)
+        need = lib.lw_hotx_build_workspace(self.cols)
+        ws = torch.empty(max(need, 1), dtype=torch.uint8, device=self.device)
+        n = ctypes.c_int32(0)
+        rc = lib.lw_hotx_build(A, max_hot, col_packed.data_ptr(), hot.data_ptr(), ctypes.byref(n),
+                               ws.data_ptr(), need, current_stream(self.device))
+        _lib.check(rc, "lw_hotx_build")
+        packed = DeviceCsr(self.rows, self.cols, self.row_offsets, col_packed[: self.nnz], self.values)
+        hx = HotColumns(packed, hot[: n.value], n.value, max_hot, self._tensor_key())
+        self.__dict__["_hotx"] = hx
+        return hx
+
+    def hot_columns(self) -> "HotColumns | None":
+        """The hot-x packing built by pack_hot_columns, if the tensors are unchanged."""
+        hx = self.__dict__.get("_hotx")
+        return hx if hx is not None and hx.key == self._tensor_key() else None
+
+    def drop_hot_columns(self) -> None:
+        self.__dict__.pop("_hotx", None)
+
+    def _tensor_key(self):
+        return (id(self.row_offsets), id(self.col_indices), id(self.values), self.rows, self.cols)
+
     def algorithmic_bytes(self) -> int:
         """SURVEY §8(d) byte model: nnz*(idx+val) + (rows+1)*off + cols*val + rows*val."""
         sv = self.values.element_size()
@@ -235,6 +277,27 @@ class Probe:
                 "atom_lane": self.atom_lane[: self.nnz].cpu().numpy(),
                 "atom_tile": self.atom_tile[: self.nnz].cpu().numpy(),
                 "atom_visits": self.atom_visits[: self.nnz].cpu().numpy()}
+
+
+@dataclass
+class HotColumns:
+    """A DeviceCsr's hot-x packing: ``packed`` is the matrix with hot columns
+    relabeled to ``slot | 0x80000000`` (csrc/hotx.cu), ``hot_cols[slot]`` the
+    original column of each slot (ascending), ``n_hot`` the slot count."""
+
+    packed: DeviceCsr
+    hot_cols: "object"   # torch int32 [n_hot]
+    n_hot: int
+    max_hot: int
+    key: tuple
+
+    def original_col_indices(self):
+        """Undo the relabeling (equals the source matrix's col_indices)."""
+        torch = _torch()
+        c = self.packed.col_indices
+        hot = c < 0
+        return torch.where(hot, self.hot_cols[(c & 0x7FFFFFFF).long().clamp_(max=max(self.n_hot - 1, 0))]
+                           if self.n_hot else c, c)
 
 
 def _offsets_tensor(ts, device):

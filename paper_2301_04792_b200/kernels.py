@@ -48,6 +48,11 @@ def _wo_workspace(rows: int, nnz: int, lanes: int, dtype_code: int) -> int:
 
 
 @functools.lru_cache(maxsize=256)
+def _hotx_workspace(rows: int, nnz: int, lanes: int, n_hot: int, dtype_code: int) -> int:
+    return _lib.load().lw_spmv_work_oriented_hotx_workspace(rows, nnz, lanes, n_hot, dtype_code)
+
+
+@functools.lru_cache(maxsize=256)
 def _mm_workspace(code: int, rows: int, nnz: int, n: int, lanes: int, dtype_code: int) -> int:
     return _lib.load().lw_spmm_workspace(code, rows, nnz, n, lanes, dtype_code)
 
@@ -62,6 +67,11 @@ def _launch(m: DeviceCsr, x, y, cfg: ExecutorConfig, probe: Probe | None, stream
     kind = cfg.schedule
     if kind is ScheduleKind.THREAD_MAPPED:
         rc = lib.lw_spmv_thread_mapped(A, xp, yp, lanes, pp, stream)
+    elif kind is ScheduleKind.MERGE_PATH and probe is None and (hx := m.hot_columns()) is not None:
+        need = _hotx_workspace(m.rows, m.nnz, lanes, hx.n_hot, A.dtype)
+        ws = _WS.get(need, m.device, stream)
+        rc = lib.lw_spmv_work_oriented_hotx(hx.packed.c_struct(), hx.hot_cols.data_ptr() if hx.n_hot else None,
+                                            hx.n_hot, xp, yp, lanes, ws.data_ptr(), ws.numel(), stream)
     elif kind is ScheduleKind.MERGE_PATH:
         need = _wo_workspace(m.rows, m.nnz, lanes, A.dtype)
         ws = _WS.get(need, m.device, stream)
