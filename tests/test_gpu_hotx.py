@@ -168,3 +168,17 @@ def test_rmat_packed_bit_identical():
     hx = m.pack_hot_columns()
     assert 0 < hx.n_hot <= 12288
     assert torch.equal(lwb.spmv(m, x, WO), y)
+
+
+def test_power_iteration_packed_iterates_bit_identical():
+    """C5's driver over a packed operand: the iterates and norms equal the unpacked run."""
+    from paper_2301_04792_b200.distributed import RowShard, nnz_balanced_bounds, power_iteration
+
+    A = lwb.generate_rmat_csr(16, 8, seed=11)
+    shard = RowShard(nnz_balanced_bounds(A.row_offsets.cpu().numpy(), 1), 0)
+    x1, n1 = power_iteration(lambda x: lwb.spmv(A, x, WO), A.rows, shard, 6, dtype=torch.float32,
+                             device="cuda")
+    A.pack_hot_columns()
+    x2, n2 = power_iteration(lambda x: lwb.spmv(A, x, WO), A.rows, shard, 6, dtype=torch.float32,
+                             device="cuda")
+    assert torch.equal(x1, x2) and n1 == n2
