@@ -264,7 +264,7 @@ def power_arm(args):
     y_local = torch.empty(A.rows, dtype=A.dtype, device=dev)
     chunks = args.chunks or (4 if world > 1 else 1)
     # hot-x packing of every SpMV operand (one-time, before warm-up)
-    hot = not args.fused and (args.hot_x == "on" or (args.hot_x == "auto" and args.dtype == "fp32"))
+    hot = args.hot_x == "on" or (args.hot_x == "auto" and args.dtype == "fp32")
     if hot:
         A.pack_hot_columns(args.max_hot or None)
     pieces = {}   # (r0, r1) -> (row-slice view, output view), built once

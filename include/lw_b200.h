@@ -176,6 +176,13 @@ int lw_spmv_work_oriented_peers(const lw_csr_t* A, const void* x, void* y, int64
                                 void* workspace, size_t workspace_bytes, int32_t n_peers,
                                 const uint64_t* peer_ptrs, uint64_t multicast_ptr,
                                 int64_t row_base, uintptr_t stream);
+/* The same over a hot-x packed matrix (lw_hotx_build): A_packed/hot_cols/n_hot
+ * as for lw_spmv_work_oriented_hotx; workspace lw_spmv_work_oriented_hotx_workspace. */
+int lw_spmv_work_oriented_peers_hotx(const lw_csr_t* A_packed, const int32_t* hot_cols,
+                                     int32_t n_hot, const void* x, void* y, int64_t lanes,
+                                     void* workspace, size_t workspace_bytes, int32_t n_peers,
+                                     const uint64_t* peer_ptrs, uint64_t multicast_ptr,
+                                     int64_t row_base, uintptr_t stream);
 
 /* Power-iteration normalisation (BASELINE C5; the reference driver's x = y/||y||):
  * lw_vector_norm writes ||y||_2 (fp64, deterministic two-level reduction) to the

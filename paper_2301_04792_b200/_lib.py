@@ -41,6 +41,7 @@ EXPORTS = (
     "lw_spmv_work_oriented",
     "lw_spmv_work_oriented_phases",
     "lw_spmv_work_oriented_peers",
+    "lw_spmv_work_oriented_peers_hotx",
     "lw_hotx_build_workspace",
     "lw_hotx_build",
     "lw_spmv_work_oriented_hotx_workspace",
@@ -137,6 +138,8 @@ _SIGNATURES = {
     "lw_spmv_work_oriented_phases": (ctypes.c_int, [_csr_p, _vp, _vp, _i64, _vp, _sz, _u32, _up]),
     "lw_spmv_work_oriented_peers": (ctypes.c_int, [_csr_p, _vp, _vp, _i64, _vp, _sz, _i32, _vp, _u64,
                                                    _i64, _up]),
+    "lw_spmv_work_oriented_peers_hotx": (ctypes.c_int, [_csr_p, _vp, _i32, _vp, _vp, _i64, _vp, _sz, _i32,
+                                                        _vp, _u64, _i64, _up]),
     "lw_hotx_build_workspace": (_sz, [_i64]),
     "lw_hotx_build": (ctypes.c_int, [_csr_p, _i32, _vp, _vp, ctypes.POINTER(_i32), _vp, _sz, _up]),
     "lw_spmv_work_oriented_hotx_workspace": (_sz, [_i64, _i64, _i64, _i32, _i32]),

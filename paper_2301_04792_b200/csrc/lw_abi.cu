@@ -25,7 +25,7 @@ size_t norm_workspace(int64_t n);
 int vector_norm(const void*, int64_t, int, void*, double*, cudaStream_t);
 int vector_scale(const void*, int64_t, int, const double*, void*, cudaStream_t);
 int spmv_work_oriented_peers(const lw_csr_t*, const void*, void*, int64_t, void*, size_t, int32_t,
-                             const uint64_t*, uint64_t, int64_t, cudaStream_t);
+                             const uint64_t*, uint64_t, int64_t, cudaStream_t, const int32_t*, int32_t);
 size_t wo_hotx_workspace(int64_t rows, int64_t nnz, int64_t lanes, int64_t n_hot, int dtype);
 int spmv_work_oriented_hotx(const lw_csr_t*, const int32_t*, int32_t, const void*, void*, int64_t, void*,
                             size_t, unsigned, cudaStream_t);
@@ -181,7 +181,21 @@ int lw_spmv_work_oriented_peers(const lw_csr_t* A, const void* x, void* y, int64
     if (A->nnz > 0 && !x) return LW_E_INVALID_ARG;
     if (lanes < 0 || (n_peers == 0 && multicast_ptr == 0)) return LW_E_INVALID_ARG;
     return spmv_work_oriented_peers(A, x, y, lanes, ws, ws_bytes, n_peers, peer_ptrs, multicast_ptr,
-                                    row_base, (cudaStream_t)stream);
+                                    row_base, (cudaStream_t)stream, nullptr, 0);
+}
+
+int lw_spmv_work_oriented_peers_hotx(const lw_csr_t* A, const int32_t* hot_cols, int32_t n_hot,
+                                     const void* x, void* y, int64_t lanes, void* ws,
+                                     size_t ws_bytes, int32_t n_peers, const uint64_t* peer_ptrs,
+                                     uint64_t multicast_ptr, int64_t row_base, uintptr_t stream) {
+    int rc = check_csr(A);
+    if (rc) return rc;
+    if (A->rows > 0 && !y) return LW_E_INVALID_ARG;
+    if (A->nnz > 0 && !x) return LW_E_INVALID_ARG;
+    if (lanes < 0 || (n_peers == 0 && multicast_ptr == 0)) return LW_E_INVALID_ARG;
+    static const int32_t none = 0;   // selects the packed kernel even with no hot slots
+    return spmv_work_oriented_peers(A, x, y, lanes, ws, ws_bytes, n_peers, peer_ptrs, multicast_ptr,
+                                    row_base, (cudaStream_t)stream, hot_cols ? hot_cols : &none, n_hot);
 }
 
 size_t lw_hotx_build_workspace(int64_t cols) { return cols < 0 ? 0 : hotx_build_workspace(cols); }

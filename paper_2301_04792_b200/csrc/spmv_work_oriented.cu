@@ -143,7 +143,9 @@ __device__ __forceinline__ void peer_store(const PeerOut& po, int64_t row, float
                      "f"(v) : "memory");
         return;
     }
-    for (int p = 0; p < po.n; ++p) reinterpret_cast<float*>(po.ptr[p])[po.base + row] = v;
+#pragma unroll   // constant indices: the pointers stay in the parameter bank (no stack copy)
+    for (int p = 0; p < LW_MAX_PEERS; ++p)
+        if (p < po.n) reinterpret_cast<float*>(po.ptr[p])[po.base + row] = v;
 }
 __device__ __forceinline__ void peer_store(const PeerOut& po, int64_t row, double v) {
     if (po.mc) {
@@ -151,7 +153,9 @@ __device__ __forceinline__ void peer_store(const PeerOut& po, int64_t row, doubl
                      "d"(v) : "memory");
         return;
     }
-    for (int p = 0; p < po.n; ++p) reinterpret_cast<double*>(po.ptr[p])[po.base + row] = v;
+#pragma unroll
+    for (int p = 0; p < LW_MAX_PEERS; ++p)
+        if (p < po.n) reinterpret_cast<double*>(po.ptr[p])[po.base + row] = v;
 }
 
 // 8 consecutive col_idx / values with 32-byte loads (sm_100 .v8.b32 / .v4.b64)
@@ -617,9 +621,9 @@ static int launch_wo(const lw_csr_t* A, const void* x, void* y, const WoPlan& p,
 }
 
 // SpMV whose rows also land in every rank's next-x buffer (fused all-gather).
-template <class OffT, class ValT>
+template <class OffT, class ValT, bool HOT>
 static int launch_wo_peers(const lw_csr_t* A, const void* x, void* y, const WoPlan& p, void* ws,
-                           const PeerOut& po, cudaStream_t s) {
+                           const PeerOut& po, cudaStream_t s, const int32_t* hot_cols, int32_t n_hot) {
     Csr<OffT, ValT> a{A->rows, A->cols, A->nnz, (const OffT*)A->row_offsets, A->col_indices,
                       (const ValT*)A->values};
     const size_t nb = (size_t)(p.lanes * p.J + 1);
@@ -632,14 +636,23 @@ static int launch_wo_peers(const lw_csr_t* A, const void* x, void* y, const WoPl
     if (rc) return rc;
     const bool vec = ((uintptr_t)A->col_indices % 32 == 0) && ((uintptr_t)A->values % 32 == 0);
     constexpr size_t smem = WoSmem<ValT>::bytes;
-    auto kern = vec ? k_wo_chunk<OffT, ValT, false, true, true> : k_wo_chunk<OffT, ValT, false, false, true>;
+    auto kern = vec ? k_wo_chunk<OffT, ValT, false, true, true, HOT>
+                    : k_wo_chunk<OffT, ValT, false, false, true, HOT>;
+    ValT* xh = nullptr;
+    if constexpr (HOT) {   // packed hot x after the carries, as in launch_wo
+        xh = (ValT*)(w + align_up(nb * 8, 256) + 2 * align_up(wo_carries(p) * 8, 256));
+        if (n_hot > 0) {
+            k_hot_pack<ValT><<<(unsigned)ceil_div(n_hot, 256), 256, 0, s>>>((const ValT*)x, hot_cols, n_hot, xh);
+            LW_LAUNCH_CHECK();
+        }
+    }
     static bool attr[2] = {false, false};
     if (!attr[vec]) {
         LW_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr[vec] = true;
     }
     kern<<<(unsigned)p.lanes, WoCfg<ValT>::NT, smem, s>>>(a, (const ValT*)x, (ValT*)y, p.items, p.J,
-                                                         tiles, c_tile, c_val, Probe{}, po, nullptr);
+                                                         tiles, c_tile, c_val, Probe{}, po, xh);
     LW_LAUNCH_CHECK();
     k_carry_fixup<ValT, true><<<ceil_div(p.lanes, 256), 256, 0, s>>>(c_tile, c_val, p.lanes, (ValT*)y,
                                                                      a.rows, po);
@@ -647,25 +660,40 @@ static int launch_wo_peers(const lw_csr_t* A, const void* x, void* y, const WoPl
     return LW_OK;
 }
 
+size_t wo_hotx_workspace(int64_t rows, int64_t nnz, int64_t lanes, int64_t n_hot, int dtype);
+
 int spmv_work_oriented_peers(const lw_csr_t* A, const void* x, void* y, int64_t lanes, void* ws,
                              size_t ws_bytes, int32_t n_peers, const uint64_t* peer_ptrs,
-                             uint64_t mc_ptr, int64_t row_base, cudaStream_t s) {
-    if (n_peers < 0 || n_peers > LW_MAX_PEERS || (n_peers > 0 && !peer_ptrs) || row_base < 0)
+                             uint64_t mc_ptr, int64_t row_base, cudaStream_t s,
+                             const int32_t* hot_cols, int32_t n_hot) {
+    if (n_peers < 0 || n_peers > LW_MAX_PEERS || (n_peers > 0 && !peer_ptrs) || row_base < 0 ||
+        n_hot < 0 || (n_hot > 0 && !hot_cols))
         return LW_E_INVALID_ARG;
     const WoPlan p = wo_plan(A->rows, A->nnz, lanes);
     if (A->rows == 0) return LW_OK;
-    if (!ws || ws_bytes < wo_workspace(A->rows, A->nnz, lanes)) return LW_E_WORKSPACE;
+    const bool hot = hot_cols != nullptr || n_hot > 0;
+    const size_t need = hot ? wo_hotx_workspace(A->rows, A->nnz, lanes, n_hot, A->dtype)
+                            : wo_workspace(A->rows, A->nnz, lanes);
+    if (!ws || ws_bytes < need) return LW_E_WORKSPACE;
     PeerOut po{};
     po.n = n_peers;
     po.base = row_base;
     po.mc = mc_ptr;
     for (int i = 0; i < n_peers; ++i) po.ptr[i] = peer_ptrs[i];
     const bool o32 = A->offset_bits == 32;
+    const int32_t* hc = hot_cols;
+    if (hot) {
+        if (A->dtype == LW_F32)
+            return o32 ? launch_wo_peers<int32_t, float, true>(A, x, y, p, ws, po, s, hc, n_hot)
+                       : launch_wo_peers<int64_t, float, true>(A, x, y, p, ws, po, s, hc, n_hot);
+        return o32 ? launch_wo_peers<int32_t, double, true>(A, x, y, p, ws, po, s, hc, n_hot)
+                   : launch_wo_peers<int64_t, double, true>(A, x, y, p, ws, po, s, hc, n_hot);
+    }
     if (A->dtype == LW_F32)
-        return o32 ? launch_wo_peers<int32_t, float>(A, x, y, p, ws, po, s)
-                   : launch_wo_peers<int64_t, float>(A, x, y, p, ws, po, s);
-    return o32 ? launch_wo_peers<int32_t, double>(A, x, y, p, ws, po, s)
-               : launch_wo_peers<int64_t, double>(A, x, y, p, ws, po, s);
+        return o32 ? launch_wo_peers<int32_t, float, false>(A, x, y, p, ws, po, s, hc, 0)
+                   : launch_wo_peers<int64_t, float, false>(A, x, y, p, ws, po, s, hc, 0);
+    return o32 ? launch_wo_peers<int32_t, double, false>(A, x, y, p, ws, po, s, hc, 0)
+               : launch_wo_peers<int64_t, double, false>(A, x, y, p, ws, po, s, hc, 0);
 }
 
 int spmv_work_oriented(const lw_csr_t* A, const void* x, void* y, int64_t lanes, void* ws,

@@ -242,8 +242,15 @@ def _spmv_peers(A, x, y, peer_ptrs, mc_ptr: int, row_base: int, ws, stream: int)
 
     lib = _lib.load()
     arr = (ctypes.c_uint64 * max(1, len(peer_ptrs)))(*[int(p) for p in peer_ptrs])
-    rc = lib.lw_spmv_work_oriented_peers(A.c_struct(), x.data_ptr(), y.data_ptr(), 0, ws.data_ptr(),
-                                         ws.numel(), len(peer_ptrs), arr, int(mc_ptr), row_base, stream)
+    hx = A.hot_columns()
+    if hx is not None:   # hot-x packed operand: same rows, bit for bit
+        rc = lib.lw_spmv_work_oriented_peers_hotx(
+            hx.packed.c_struct(), hx.hot_cols.data_ptr() if hx.n_hot else None, hx.n_hot,
+            x.data_ptr(), y.data_ptr(), 0, ws.data_ptr(), ws.numel(), len(peer_ptrs), arr,
+            int(mc_ptr), row_base, stream)
+    else:
+        rc = lib.lw_spmv_work_oriented_peers(A.c_struct(), x.data_ptr(), y.data_ptr(), 0, ws.data_ptr(),
+                                             ws.numel(), len(peer_ptrs), arr, int(mc_ptr), row_base, stream)
     _lib.check(rc, "lw_spmv_work_oriented_peers")
 
 
@@ -291,7 +298,10 @@ def power_iteration_fused(A, n: int, shard: RowShard, iters: int, group=None, x0
     y_local = torch.empty(max(A.rows, 1), dtype=dtype, device=dev)
     from . import _lib
 
-    need = _lib.load().lw_spmv_work_oriented_workspace(A.rows, A.nnz, 0, A.c_struct().dtype)
+    hx = A.hot_columns()
+    need = (_lib.load().lw_spmv_work_oriented_hotx_workspace(A.rows, A.nnz, 0, hx.n_hot, A.c_struct().dtype)
+            if hx is not None else
+            _lib.load().lw_spmv_work_oriented_workspace(A.rows, A.nnz, 0, A.c_struct().dtype))
     ws = Workspace().get(need, dev)
     stream = current_stream(dev)
     norms = []

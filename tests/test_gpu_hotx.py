@@ -182,3 +182,18 @@ def test_power_iteration_packed_iterates_bit_identical():
     x2, n2 = power_iteration(lambda x: lwb.spmv(A, x, WO), A.rows, shard, 6, dtype=torch.float32,
                              device="cuda")
     assert torch.equal(x1, x2) and n1 == n2
+
+
+def test_fused_power_iteration_packed_bit_identical():
+    """The SpMV-with-peer-writes kernel over a packed operand (world 1: the rank's own
+    next-x buffer is its only peer) gives the unpacked iterates exactly."""
+    from paper_2301_04792_b200.distributed import (RowShard, nnz_balanced_bounds,
+                                                   power_iteration_fused)
+
+    A = lwb.generate_rmat_csr(16, 8, seed=12)
+    shard = RowShard(nnz_balanced_bounds(A.row_offsets.cpu().numpy(), 1), 0)
+    x1, n1 = power_iteration_fused(A, A.rows, shard, 6)
+    A.pack_hot_columns()
+    x2, n2 = power_iteration_fused(A, A.rows, shard, 6)
+    torch.cuda.synchronize()
+    assert torch.equal(x1, x2) and n1 == n2
