@@ -25,6 +25,7 @@
 //    per lane running the reference's member loop over global memory, with a
 //    monotone tile advance (_fast.py:75-76) and atomic adds into a zeroed y (the
 //    reference's pre-zeroed y += v*x, kernels.py:63 / _fast.py:77).
+#include <algorithm>
 #include <climits>
 #include <type_traits>
 
@@ -89,10 +90,148 @@ __device__ __forceinline__ void gather_loaded(const StepLoads<ValT, U>& L, const
 }
 
 // ---- warp tiles -------------------------------------------------------------------
+#ifndef LW_GW_CAP      // atoms per warp block staged in shared memory (0 = off)
+#define LW_GW_CAP 576
+#endif
+#ifndef LW_GW_SU       // member-stride steps in flight on the staged path
+#define LW_GW_SU 2
+#endif
+constexpr int GW_SU = LW_GW_SU;
+#ifndef LW_GW_LONG     // longest row the staged path sums in one lane
+#define LW_GW_LONG 128
+#endif
+constexpr int GW_LONG = LW_GW_LONG;
 #ifndef LW_GW_MINB
 #define LW_GW_MINB 0
 #endif
+// The staged-block path of k_group_warp (see the kernel).
+template <class OffT, class ValT, int CAP>
+__device__ __forceinline__ void group_warp_staged(const Csr<OffT, ValT>& A, const ValT* __restrict__ x,
+                                               ValT* __restrict__ y, int64_t tb, int tc, int64_t base,
+                                               OffT excl, OffT incl, OffT cnt, ValT* sp) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    int ta = 0;
+    while (ta < tc) {
+        const OffT sa = shfl(excl, ta);
+        // tiles ta .. te-1 whose atoms end within sa + CAP (incl is increasing)
+        const unsigned fit = __ballot_sync(0xffffffffu, lane >= ta && lane < tc && incl - sa <= (OffT)CAP);
+        const int te = 32 - __clz(fit);
+        const OffT sb = shfl(incl, te - 1);
+        for (OffT k0 = sa & ~(OffT)(kWarp - 1); k0 < sb; k0 += GW_SU * kWarp) {
+            int32_t c[GW_SU];
+            ValT v[GW_SU];
+#pragma unroll
+            for (int u = 0; u < GW_SU; ++u) {
+                const OffT k = k0 + u * kWarp + lane;
+                const bool valid = k >= sa && k < sb;
+                c[u] = valid ? ld_stream(A.col + base + k) : 0;
+                v[u] = valid ? ld_stream(A.val + base + k) : (ValT)0;
+            }
+#pragma unroll
+            for (int u = 0; u < GW_SU; ++u) {
+                const OffT k = k0 + u * kWarp + lane;
+                if (k >= sa && k < sb) sp[k - sa] = v[u] * ld_gather(x + c[u]);
+            }
+        }
+        __syncwarp();
+        if (lane >= ta && lane < te) {
+            double acc = 0.0;
+            const int e0 = (int)(excl - sa), n = (int)cnt;
+            for (int j = 0; j < n; ++j) acc += (double)sp[e0 + j];
+            y[tb + lane] = (ValT)acc;
+        }
+        __syncwarp();
+        ta = te;
+    }
+}
+
+// The cooperative path of k_group_warp (blocks with long rows, and every block of
+// the instrumented variant).
 template <class OffT, class ValT, bool PROBE>
+__device__ __forceinline__ void group_warp_coop(const Csr<OffT, ValT>& A, const ValT* __restrict__ x,
+                                             ValT* __restrict__ y, const Probe& probe, int64_t tb,
+                                             int tc, int64_t base, OffT cnt, OffT excl, OffT total,
+                                             int64_t glane, int64_t& mine, double* acc) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    acc[lane] = 0.0;
+    __syncwarp();
+    // U member-stride steps per iteration (lane takes local atoms k0+u*32+lane),
+    // all their loads and gathers in flight before the first reduction; U = GU
+    // only for long blocks (short ones would waste the padded steps)
+    int t_cur = 0;   // tile of the previous step's last atom (warp-uniform)
+    auto steps = [&](auto uc) {
+      constexpr int U = decltype(uc)::value;
+      StepLoads<ValT, U> cur, nxt;
+      if (U > 1) load_steps<ValT, U, kWarp>(A, base, (OffT)0, lane, total, cur);
+      for (OffT k0 = 0; k0 < total; k0 += U * kWarp) {
+        double p[U];
+        if (U > 1) {   // long block: next steps' loads overlap these gathers
+            load_steps<ValT, U, kWarp>(A, base, (OffT)(k0 + U * kWarp), lane, total, nxt);
+            gather_loaded<ValT, U, kWarp>(cur, x, k0, lane, total, p);
+            cur = nxt;
+        } else {
+            gather_steps<ValT, U, kWarp>(A, x, base, k0, lane, total, p);
+        }
+        // non-empty tiles starting inside this step's atoms (lane j <-> tile j)
+        const uint32_t starts = U == 1 ? __ballot_sync(
+            0xffffffffu, lane < tc && cnt > 0 && excl >= k0 && excl < k0 + (OffT)kWarp) : 0u;
+        const int t_it = t_cur;
+        int t_next = t_cur;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const OffT k = k0 + u * kWarp + lane;
+            const bool valid = k < total;
+            // get_tile (largest non-empty t with excl[t] <= k): the step's atoms
+            // are consecutive, so only the non-empty tiles that START inside the
+            // step can change the tile; lane j flags tile j, and the few flagged
+            // starts are broadcast in order (one shuffle each, none inside a
+            // long row) instead of a 5-probe search per atom
+            // (long blocks, U > 1, keep the independent 5-probe search: there the
+            // steps' searches overlap, and R-MAT / power-law blocks measured 15-25%
+            // slower with the start-following loop)
+            int t = 0;
+            if (U == 1) {
+                t = t_it;
+                for (uint32_t sm = starts; sm; sm &= sm - 1) {
+                    const int j = __ffs(sm) - 1;
+                    if (k >= shfl(excl, j)) t = j;
+                }
+                t_next = shfl(t, kWarp - 1);
+            } else {
+#pragma unroll
+                for (int s = kWarp / 2; s >= 1; s >>= 1) {
+                    const OffT e = shfl(excl, t + s);
+                    if (t + s < tc && e <= k) t += s;
+                }
+            }
+            if (PROBE && valid) { probe_atom(probe, base + k, glane, tb + t); ++mine; }
+            const int key = valid ? t : INT_MAX;
+            const int prev = shfl_up(key, 1);
+            const bool head = lane == 0 || prev != key;
+            const uint32_t heads = __ballot_sync(0xffffffffu, head);
+            // a step's partial sums (<= 32 products) in the value precision
+            const double sum = (double)warp_segsum_heads<ValT>((ValT)p[u], lane, heads);
+            if (valid && head) acc[t] += sum;
+            __syncwarp();
+        }
+        t_cur = t_next;
+      }
+    };
+    if (total >= (OffT)(GU_LONG * kWarp)) steps(std::integral_constant<int, GU>{});
+    else steps(std::integral_constant<int, 1>{});
+    if (lane < tc) y[tb + lane] = (ValT)acc[lane];
+    __syncwarp();
+}
+
+// MODE: GW_ALL runs every block through the cooperative path (the instrumented
+// variant); the uninstrumented SpMV is two launches over the same groups and
+// blocks, GW_STAGED (blocks whose rows are all <= GW_LONG atoms, staged) then
+// GW_COOP (the other blocks, cooperative). Each block is computed by one of them
+// in full, so y does not depend on which warp ran it; the two paths are separate
+// kernels because inlined together they cost the cooperative loop its register
+// allocation (C3 12.1 -> 17.3 ms, and 24 ms as a non-inlined call).
+constexpr int GW_ALL = 0, GW_STAGED = 1, GW_COOP = 2;
+template <class OffT, class ValT, bool PROBE, int MODE = GW_ALL>
 __global__ void __launch_bounds__(256, LW_GW_MINB)
     k_group_warp(Csr<OffT, ValT> A, const ValT* __restrict__ x, ValT* __restrict__ y,
                  int64_t groups, Probe probe) {
@@ -119,74 +258,36 @@ __global__ void __launch_bounds__(256, LW_GW_MINB)
         const OffT excl = incl - cnt;
         const OffT total = shfl(incl, kWarp - 1);
         const int64_t base = (int64_t)shfl(lo_off, 0);
-        s_acc[warp][lane] = 0.0;
-        __syncwarp();
-        // U member-stride steps per iteration (lane takes local atoms k0+u*32+lane),
-        // all their loads and gathers in flight before the first reduction; U = GU
-        // only for long blocks (short ones would waste the padded steps)
-        int t_cur = 0;   // tile of the previous step's last atom (warp-uniform)
-        auto steps = [&](auto uc) {
-          constexpr int U = decltype(uc)::value;
-          StepLoads<ValT, U> cur, nxt;
-          if (U > 1) load_steps<ValT, U, kWarp>(A, base, (OffT)0, lane, total, cur);
-          for (OffT k0 = 0; k0 < total; k0 += U * kWarp) {
-            double p[U];
-            if (U > 1) {   // long block: next steps' loads overlap these gathers
-                load_steps<ValT, U, kWarp>(A, base, (OffT)(k0 + U * kWarp), lane, total, nxt);
-                gather_loaded<ValT, U, kWarp>(cur, x, k0, lane, total, p);
-                cur = nxt;
-            } else {
-                gather_steps<ValT, U, kWarp>(A, x, base, k0, lane, total, p);
+        if constexpr (MODE != GW_ALL) {
+            // Staged block (rows up to GW_LONG atoms): the members compute their
+            // atoms' products exactly as the schedule assigns them (member m: local
+            // atoms m, m+32, ..., GW_SU steps of loads in flight) into shared memory,
+            // one tile-aligned segment of <= CAP atoms at a time, and the lane owning
+            // tile t then sums the tile's products in atom order (fp64). No per-atom
+            // get_tile and no per-step segmented reduction; integer data stays
+            // bit-exact (same products, exact fp64 sums). Blocks with a longer row
+            // take the cooperative path (one lane would serialise the row).
+            constexpr int CAP = LW_GW_CAP > 0 ? LW_GW_CAP * 4 / (int)sizeof(ValT) : 1;
+            OffT mx = cnt;
+#pragma unroll
+            for (int d = 16; d >= 1; d >>= 1) {
+                const OffT o = __shfl_xor_sync(0xffffffffu, mx, d);
+                mx = o > mx ? o : mx;
             }
-            // non-empty tiles starting inside this step's atoms (lane j <-> tile j)
-            const uint32_t starts = U == 1 ? __ballot_sync(
-                0xffffffffu, lane < tc && cnt > 0 && excl >= k0 && excl < k0 + (OffT)kWarp) : 0u;
-            const int t_it = t_cur;
-            int t_next = t_cur;
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const OffT k = k0 + u * kWarp + lane;
-                const bool valid = k < total;
-                // get_tile (largest non-empty t with excl[t] <= k): the step's atoms
-                // are consecutive, so only the non-empty tiles that START inside the
-                // step can change the tile; lane j flags tile j, and the few flagged
-                // starts are broadcast in order (one shuffle each, none inside a
-                // long row) instead of a 5-probe search per atom
-                // (long blocks, U > 1, keep the independent 5-probe search: there the
-                // steps' searches overlap, and R-MAT / power-law blocks measured 15-25%
-                // slower with the start-following loop)
-                int t = 0;
-                if (U == 1) {
-                    t = t_it;
-                    for (uint32_t sm = starts; sm; sm &= sm - 1) {
-                        const int j = __ffs(sm) - 1;
-                        if (k >= shfl(excl, j)) t = j;
-                    }
-                    t_next = shfl(t, kWarp - 1);
-                } else {
-#pragma unroll
-                    for (int s = kWarp / 2; s >= 1; s >>= 1) {
-                        const OffT e = shfl(excl, t + s);
-                        if (t + s < tc && e <= k) t += s;
-                    }
+            const bool staged = mx <= (OffT)(GW_LONG < CAP ? GW_LONG : CAP);
+            if constexpr (MODE == GW_STAGED) {
+                if (staged) {
+                    __shared__ ValT s_prod[8][CAP];
+                    group_warp_staged<OffT, ValT, CAP>(A, x, y, tb, tc, base, excl, incl, cnt,
+                                                       s_prod[warp]);
                 }
-                if (PROBE && valid) { probe_atom(probe, base + k, glane, tb + t); ++mine; }
-                const int key = valid ? t : INT_MAX;
-                const int prev = shfl_up(key, 1);
-                const bool head = lane == 0 || prev != key;
-                const uint32_t heads = __ballot_sync(0xffffffffu, head);
-                // a step's partial sums (<= 32 products) in the value precision
-                const double sum = (double)warp_segsum_heads<ValT>((ValT)p[u], lane, heads);
-                if (valid && head) s_acc[warp][t] += sum;
-                __syncwarp();
+                continue;
+            } else {
+                if (staged) continue;
             }
-            t_cur = t_next;
-          }
-        };
-        if (total >= (OffT)(GU_LONG * kWarp)) steps(std::integral_constant<int, GU>{});
-        else steps(std::integral_constant<int, 1>{});
-        if (lane < tc) y[tb + lane] = (ValT)s_acc[warp][lane];
-        __syncwarp();
+        }
+        group_warp_coop<OffT, ValT, PROBE>(A, x, y, probe, tb, tc, base, cnt, excl, total, glane, mine,
+                                           s_acc[warp]);
     }
     if (PROBE && probe.lane_atoms) probe.lane_atoms[glane] = mine;
 }
@@ -335,7 +436,11 @@ static int64_t groups_per_sm(int64_t gs, int64_t tpb) {
 #endif
     if (LW_GROUP_OCC) {
         if (gs == 32 && tpb == 32) {
-            static const int64_t w = resident_ctas(k_group_warp<int32_t, float, false>, 256) * 8;
+            // both launches of the staged/cooperative pair run the same groups: size
+            // them to the kernel with fewer resident CTAs, one wave for each
+            static const int64_t w = std::min(
+                resident_ctas(k_group_warp<int32_t, float, false, (LW_GW_CAP > 0 ? GW_STAGED : GW_ALL)>, 256),
+                resident_ctas(k_group_warp<int32_t, float, false, (LW_GW_CAP > 0 ? GW_COOP : GW_ALL)>, 256)) * 8;
             if (w > 0) return w;
         } else if (gs == tpb && gs == 256) {
             static const int64_t b = resident_ctas(k_group_block<int32_t, float, 256, false>, 256);
@@ -374,8 +479,17 @@ static int launch_group(const lw_csr_t* A, const void* x, void* y, int64_t lanes
         case GK_WARP: {
             const int64_t groups = lanes / 32;
             const int64_t grid = ceil_div(groups, 8);
-            if (probe) k_group_warp<OffT, ValT, true><<<grid, 256, 0, s>>>(a, xv, yv, groups, p);
-            else       k_group_warp<OffT, ValT, false><<<grid, 256, 0, s>>>(a, xv, yv, groups, p);
+            if (probe) {
+                k_group_warp<OffT, ValT, true><<<grid, 256, 0, s>>>(a, xv, yv, groups, p);
+            } else if (LW_GW_CAP > 0 && ceil_div(A->rows, 32) >= 4 * (int64_t)sm_count()) {
+                // (a few hundred blocks: one launch of the cooperative kernel is faster,
+                // C1 0.053 vs 0.087 ms for the staged/cooperative pair)
+                k_group_warp<OffT, ValT, false, GW_STAGED><<<grid, 256, 0, s>>>(a, xv, yv, groups, p);
+                LW_LAUNCH_CHECK();
+                k_group_warp<OffT, ValT, false, GW_COOP><<<grid, 256, 0, s>>>(a, xv, yv, groups, p);
+            } else {
+                k_group_warp<OffT, ValT, false><<<grid, 256, 0, s>>>(a, xv, yv, groups, p);
+            }
             break;
         }
         case GK_BLOCK: {

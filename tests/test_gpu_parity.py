@@ -473,3 +473,26 @@ def test_power_iteration_graph_replay_matches_eager():
         x2, n2 = run()
         torch.cuda.synchronize()
         assert torch.equal(x1, x2) and n1 == n2
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_group_warp_staged_and_cooperative_blocks_bit_exact(dtype):
+    """Large enough for the staged/cooperative launch pair of the warp-tile kernel
+    (>= 4 blocks per SM): short-row blocks (several shared-memory segments when a
+    block holds more atoms than one segment), blocks with rows near the staged
+    limit, and blocks with rows beyond it; integer data, so y is exact."""
+    rng = np.random.default_rng(5)
+    rows, cols = 40_000, 30_000
+    lens = rng.integers(0, 41, size=rows)
+    lens[::97] = rng.integers(100, 129, size=len(lens[::97]))
+    lens[::1000] = 500
+    lens[5000:5032] = 33   # one block of exactly 1056 atoms
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    col = np.concatenate([np.sort(rng.choice(cols, size=int(n), replace=False)) for n in lens])
+    val = rng.integers(-3, 4, size=len(col)).astype(np.float64)
+    x = rng.integers(-3, 4, size=cols).astype(np.float64)
+    want = oracle.spmv(off, col, val, x, "thread-mapped", lanes=1)
+    m = dev_csr(off, col, val, cols, dtype)
+    for lanes in (None, 32 * 700, 32 * 5000):
+        np.testing.assert_array_equal(run(m, x, "group-mapped", lanes, 32, 32), want,
+                                      err_msg=f"lanes={lanes}")
