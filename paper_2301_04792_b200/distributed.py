@@ -285,18 +285,24 @@ def power_iteration_fused(A, n: int, shard: RowShard, iters: int, group=None, x0
         import torch.distributed._symmetric_memory as symm_mem
 
         g = group or dist.group.WORLD
+        me = dist.get_rank(g)
         bufs = [symm_mem.empty(n, dtype=dtype, device=dev) for _ in range(2)]
         hdls = [symm_mem.rendezvous(b, g) for b in bufs]
-        peers = [list(h.buffer_ptrs) for h in hdls]
+        # the rank's own rows are the kernel's y (its slice of its own buffer); the
+        # peer stores go to the other ranks' buffers only
+        peers = [[p for i, p in enumerate(h.buffer_ptrs) if i != me] for h in hdls]
         mcs = [int(getattr(h, "multicast_ptr", 0) or 0) if multicast else 0 for h in hdls]
     else:
         bufs = [torch.empty(n, dtype=dtype, device=dev) for _ in range(2)]
         hdls = [None, None]
-        peers = [[b.data_ptr()] for b in bufs]
+        peers = [[], []]
         mcs = [0, 0]
     x = torch.full((n,), 1.0 / np.sqrt(n), dtype=dtype, device=dev) if x0 is None else x0
-    y_local = torch.empty(max(A.rows, 1), dtype=dtype, device=dev)
     from . import _lib
+    from .kernels import spmv as _spmv
+    from .executor import ExecutorConfig
+    from .schedules import ScheduleKind
+    wo = ExecutorConfig(schedule=ScheduleKind.MERGE_PATH)
 
     hx = A.hot_columns()
     need = (_lib.load().lw_spmv_work_oriented_hotx_workspace(A.rows, A.nnz, 0, hx.n_hot, A.c_struct().dtype)
@@ -307,7 +313,11 @@ def power_iteration_fused(A, n: int, shard: RowShard, iters: int, group=None, x0
     norms = []
     for k in range(iters):
         b = k % 2
-        _spmv_peers(A, x, y_local, peers[b], mcs[b], shard.r0, ws, stream)
+        y_own = bufs[b][shard.r0: shard.r1]
+        if peers[b] or mcs[b]:
+            _spmv_peers(A, x, y_own, peers[b], mcs[b], shard.r0, ws, stream)
+        else:   # nobody to send to (world 1): the SpMV writes the next x directly
+            _spmv(A, x, wo, out=y_own)
         if hdls[b] is not None:
             hdls[b].barrier(channel=0)
         nrm, x = _normalise(bufs[b], dtype)

@@ -197,3 +197,31 @@ def test_fused_power_iteration_packed_bit_identical():
     x2, n2 = power_iteration_fused(A, A.rows, shard, 6)
     torch.cuda.synchronize()
     assert torch.equal(x1, x2) and n1 == n2
+
+
+def test_peers_hotx_kernel_writes_every_buffer_at_the_row_base():
+    """lw_spmv_work_oriented_peers_hotx: the packed peers kernel writes y and every peer
+    buffer at row_base with the unpacked kernel's rows, bit for bit."""
+    import ctypes
+
+    from paper_2301_04792_b200 import _lib
+
+    A = lwb.generate_rmat_csr(15, 8, seed=4)
+    x = torch.rand(A.cols, device="cuda")
+    want = lwb.spmv(A, x, WO)
+    hx = A.pack_hot_columns()
+    bufs = [torch.full((A.rows + 50,), -7.0, device="cuda") for _ in range(2)]
+    y = torch.empty(A.rows, device="cuda")
+    lib = _lib.load()
+    need = lib.lw_spmv_work_oriented_hotx_workspace(A.rows, A.nnz, 0, hx.n_hot, _lib.LW_F32)
+    ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+    ptrs = (ctypes.c_uint64 * 2)(*[b.data_ptr() for b in bufs])
+    rc = lib.lw_spmv_work_oriented_peers_hotx(hx.packed.c_struct(), hx.hot_cols.data_ptr(), hx.n_hot,
+                                              x.data_ptr(), y.data_ptr(), 0, ws.data_ptr(), need, 2,
+                                              ptrs, 0, 25, torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    torch.cuda.synchronize()
+    assert torch.equal(y, want)
+    for b in bufs:
+        assert torch.equal(b[25:25 + A.rows], want)
+        assert (b[:25] == -7.0).all() and (b[25 + A.rows:] == -7.0).all()
