@@ -347,7 +347,8 @@ def power_arm(args):
         "breakdown_ms": None if (args.fused or args.graph) else {"spmv_max_rank": round(spmv_ms, 3),
                                                  "allgather_normalise": round(ms - spmv_ms, 3)},
         "final_norm": norms[-1] if norms else None,
-        "gpu_launches": ((3 + hot) * (1 if args.fused else chunks) + 3) * args.iters * args.steps,
+        "gpu_launches": ((3 + (hot and args.fused and world > 1)) * (1 if args.fused else chunks) + 3)
+                        * args.iters * args.steps,
         "clocks": clocks.summary(),
     }
     if rank == 0:
@@ -547,14 +548,14 @@ def our_arm(args):
                      "achieved_gather_every_nnz": round(gather_bytes / (kern_ms * 1e-3) / 1e9, 1),
                      "frac_gather_every_nnz": round(gather_bytes / (kern_ms * 1e-3) / 1e9 / hbm, 4)},
         "hbm_gbs_step": round(alg_bytes / (ms * 1e-3) / 1e9, 1),
-        "gpu_launches": (launches_per_step + (hx is not None)) * args.steps,
+        "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks.summary(),
     }
     if hx is not None:
         line["config"]["x_layout"] = (f"hot-x packed: {hx.n_hot} most gathered columns in a dense "
                                       f"per-call copy kept in L1 (DESIGN.md 4e); one-time inspector "
                                       f"{hx_build_ms:.1f} ms outside the timed region")
-        line["roofline"]["kernel"] = "k_hot_pack + k_wo_chunk"
+        line["roofline"]["kernel"] = "k_wo_chunk (hot-x packed; the pack rides on the partition launch)"
         line["unpacked"] = {"ms_per_step": round(ms_unpacked, 4), "kernel_ms": round(kern_unpacked, 4),
                             "value": round(2.0 * nnz_total / (ms_unpacked * 1e-3) / 1e9, 3),
                             "frac": round(alg_bytes / (kern_unpacked * 1e-3) / 1e9 / hbm, 4),

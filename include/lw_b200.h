@@ -156,8 +156,9 @@ int lw_spmv_work_oriented_hotx(const lw_csr_t* A_packed, const int32_t* hot_cols
                                const void* x, void* y, int64_t lanes, void* workspace,
                                size_t workspace_bytes, uintptr_t stream);
 
-/* The same in three stream-ordered phases (bit 0 partition, bit 1 pack + SpMV
- * chunk kernel, bit 2 carry fix-up), as lw_spmv_work_oriented_phases. */
+/* The same in three stream-ordered phases (bit 0: partition + pack of x into the
+ * workspace's hot slots, one launch; bit 1: SpMV chunk kernel; bit 2: carry
+ * fix-up), as lw_spmv_work_oriented_phases; phases 1 and 2 must see the same x. */
 int lw_spmv_work_oriented_hotx_phases(const lw_csr_t* A_packed, const int32_t* hot_cols,
                                       int32_t n_hot, const void* x, void* y, int64_t lanes,
                                       void* workspace, size_t workspace_bytes,

@@ -484,6 +484,31 @@ __global__ void k_hot_pack(const ValT* __restrict__ x, const int32_t* __restrict
     if (i < n_hot) xh[i] = x[hot_cols[i]];
 }
 
+// The partition search and the hot-x pack are independent; one launch runs both
+// (blocks [0, nsb) search, the rest pack), so the packed path adds no launch.
+template <class OffT, class ValT>
+__global__ void k_search_pack(const OffT* __restrict__ off, int64_t rows, int64_t nnz,
+                              int64_t n_bounds, int64_t J, int64_t items, int64_t S,
+                              int64_t* __restrict__ out_tile, unsigned nsb,
+                              const ValT* __restrict__ x, const int32_t* __restrict__ hot_cols,
+                              int32_t n_hot, ValT* __restrict__ xh) {
+    if (blockIdx.x >= nsb) {
+        const int i = (int)(blockIdx.x - nsb) * blockDim.x + threadIdx.x;
+        if (i < n_hot) xh[i] = x[hot_cols[i]];
+        return;
+    }
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n_bounds) return;
+    const int64_t d = wo_bound_diag(k, J, items, S, rows + nnz);
+    int64_t lo = max((int64_t)0, d - nnz), hi = min(d, rows);
+    while (lo < hi) {   // greatest t with off[t] <= d - t, as k_merge_path_search
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (ld_off(off + mid) <= d - mid) lo = mid;
+        else hi = mid - 1;
+    }
+    out_tile[k] = lo;
+}
+
 // ---- host side -------------------------------------------------------------------
 struct WoPlan {
     int64_t total, lanes, items, J;
@@ -587,7 +612,15 @@ static int launch_wo(const lw_csr_t* A, const void* x, void* y, const WoPlan& p,
     const bool vec = ((uintptr_t)A->col_indices % 32 == 0) && ((uintptr_t)A->values % 32 == 0);
     const int64_t n_carry = p.lanes;   // the fix-up walks one carry per lane
 
-    if (phases & WO_PHASE_PARTITION) {
+    if ((phases & WO_PHASE_PARTITION) && hot_cols && n_hot > 0) {   // partition + hot-x pack
+        ValT* xh = (ValT*)(w + align_up(nb * 8, 256) + 2 * align_up(nc * 8, 256));
+        const unsigned nsb = (unsigned)ceil_div((int64_t)nb, 256);
+        const unsigned npb = (unsigned)ceil_div(n_hot, 256);
+        k_search_pack<OffT, ValT><<<nsb + npb, 256, 0, s>>>(a.off, a.rows, a.nnz, (int64_t)nb, p.J, p.items,
+                                                          WO_S, tiles, nsb, (const ValT*)x, hot_cols,
+                                                          n_hot, xh);
+        LW_LAUNCH_CHECK();
+    } else if (phases & WO_PHASE_PARTITION) {
         int rc = launch_search<OffT>(a.off, a.rows, a.nnz, (int64_t)nb, p.J, p.items, WO_S, tiles,
                                      nullptr, s);
         if (rc) return rc;
@@ -600,10 +633,7 @@ static int launch_wo(const lw_csr_t* A, const void* x, void* y, const WoPlan& p,
         int rc = LW_OK;
         if (hot_cols) {   // packed hot x lives after the carries in the workspace
             ValT* xh = (ValT*)(w + align_up(nb * 8, 256) + 2 * align_up(nc * 8, 256));
-            if (n_hot > 0) {
-                k_hot_pack<ValT><<<(unsigned)ceil_div(n_hot, 256), 256, 0, s>>>(xv, hot_cols, n_hot, xh);
-                LW_LAUNCH_CHECK();
-            }
+            // (xh was packed by the partition phase's launch, k_search_pack)
             rc = vec ? launch_chunk<OffT, ValT, false, true, true>(a, xv, yv, p, tiles, c_tile, c_val, pr, s, xh)
                      : launch_chunk<OffT, ValT, false, false, true>(a, xv, yv, p, tiles, c_tile, c_val, pr, s, xh);
         } else if (P) rc = vec ? launch_chunk<OffT, ValT, true, true>(a, xv, yv, p, tiles, c_tile, c_val, pr, s)
