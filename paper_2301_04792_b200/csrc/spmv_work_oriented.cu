@@ -137,25 +137,37 @@ struct PeerOut {
     uint64_t mc;                    // multicast base address, 0 = none
 };
 
-__device__ __forceinline__ void peer_store(const PeerOut& po, int64_t row, float v) {
+template <bool SP = false>   // SP: peer bases from shared memory (a runtime-bounded loop)
+__device__ __forceinline__ void peer_store(const PeerOut& po, const uint64_t* sptr, int64_t row, float v) {
     if (po.mc) {
         asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(po.mc + (uint64_t)(po.base + row) * 4),
                      "f"(v) : "memory");
         return;
     }
+    if constexpr (SP) {
+#pragma unroll 1
+        for (int p = 0; p < po.n; ++p) reinterpret_cast<float*>(sptr[p])[po.base + row] = v;
+    } else {
 #pragma unroll   // constant indices: the pointers stay in the parameter bank (no stack copy)
-    for (int p = 0; p < LW_MAX_PEERS; ++p)
-        if (p < po.n) reinterpret_cast<float*>(po.ptr[p])[po.base + row] = v;
+        for (int p = 0; p < LW_MAX_PEERS; ++p)
+            if (p < po.n) reinterpret_cast<float*>(po.ptr[p])[po.base + row] = v;
+    }
 }
-__device__ __forceinline__ void peer_store(const PeerOut& po, int64_t row, double v) {
+template <bool SP = false>   // SP: peer bases from shared memory (a runtime-bounded loop)
+__device__ __forceinline__ void peer_store(const PeerOut& po, const uint64_t* sptr, int64_t row, double v) {
     if (po.mc) {
         asm volatile("multimem.st.relaxed.sys.global.f64 [%0], %1;" ::"l"(po.mc + (uint64_t)(po.base + row) * 8),
                      "d"(v) : "memory");
         return;
     }
+    if constexpr (SP) {
+#pragma unroll 1
+        for (int p = 0; p < po.n; ++p) reinterpret_cast<double*>(sptr[p])[po.base + row] = v;
+    } else {
 #pragma unroll
-    for (int p = 0; p < LW_MAX_PEERS; ++p)
-        if (p < po.n) reinterpret_cast<double*>(po.ptr[p])[po.base + row] = v;
+        for (int p = 0; p < LW_MAX_PEERS; ++p)
+            if (p < po.n) reinterpret_cast<double*>(po.ptr[p])[po.base + row] = v;
+    }
 }
 
 // 8 consecutive col_idx / values with 32-byte loads (sm_100 .v8.b32 / .v4.b64)
@@ -276,6 +288,11 @@ __global__ void __launch_bounds__(WoCfg<ValT>::NT)
     ValT* s_seg = reinterpret_cast<ValT*>(sm + SM::seg_off);
     uint32_t* s_flag = reinterpret_cast<uint32_t*>(sm + SM::flag_off);
     __shared__ WoScan<NT> scan;
+    __shared__ uint64_t s_peer[PEERS && HOT ? LW_MAX_PEERS : 1];   // peer bases (packed variant)
+    if (PEERS && HOT && threadIdx.x == 0) {
+#pragma unroll   // constant indices keep the parameter struct in the constant bank
+        for (int p = 0; p < LW_MAX_PEERS; ++p) s_peer[p] = po.ptr[p];
+    }
 
     const int tid = threadIdx.x, lane = tid & (kWarp - 1), warp = tid >> 5;
     const int64_t l = blockIdx.x;
@@ -411,7 +428,7 @@ __global__ void __launch_bounds__(WoCfg<ValT>::NT)
             double v = e > st ? (double)s_seg[e - 1] : 0.0;
             if (i == 0 && run_has && run_row == t0) v += run_val;
             y[t0 + i] = (ValT)v;
-            if (PEERS) peer_store(po, t0 + i, (ValT)v);
+            if (PEERS) peer_store<HOT>(po, s_peer, t0 + i, (ValT)v);   // smem bases: packed 1.24 -> 1.18 ms, unpacked 1.30 -> 1.50 (kept on the constant bank)
         }
         if (PROBE) {
             for (int w = tid; w < n_atoms; w += NT) {
@@ -473,7 +490,7 @@ __global__ void k_carry_fixup(const int64_t* __restrict__ carry_tile,
     }
     const ValT v = (ValT)((double)y[r] + s);
     y[r] = v;
-    if (PEERS) peer_store(po, r, v);
+    if (PEERS) peer_store(po, po.ptr, r, v);
 }
 
 // ---- 4. hot-x pack: xh[slot] = x[hot_cols[slot]] (n_hot gathers per call) ----------------
