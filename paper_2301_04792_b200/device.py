@@ -166,6 +166,9 @@ class DeviceCsr:
         12288 fp32 / 6144 fp64) get dense slots of a per-call packed x that the
         kernel keeps in L1; y stays bit-identical to the unpacked kernel. Costs
         one int32 copy of col_indices. Synchronizes the current stream once.
+        The packing shares row_offsets / values with the matrix and follows
+        tensor replacement (a new col_indices tensor drops it), but an in-place
+        edit of col_indices is not seen: call drop_hot_columns() after one.
         """
         torch = _torch()
         if max_hot is None:
