@@ -415,6 +415,9 @@ def our_arm(args):
     ws_bytes = lib.lw_spmv_workspace(_lib.LW_MERGE_PATH, A.rows, A.nnz, 0, Ac.dtype)
     ws = torch.empty(max(ws_bytes, 256), dtype=torch.uint8, device=dev)
     launches_per_step = 3 if sched is lwb.ScheduleKind.MERGE_PATH else 1
+    if args.schedule == "group_warp":   # staged + cooperative pair on >= 4 blocks per SM
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        launches_per_step = 2 if -(-A.rows // 32) >= 4 * sms else 1
     lanes = 0
     if args.items and sched is lwb.ScheduleKind.MERGE_PATH:
         lanes = -(-(A.rows + A.nnz) // args.items)
