@@ -75,3 +75,25 @@ def test_workspace_query_scales_with_lanes(lib):
     auto = lib.lw_spmv_work_oriented_workspace(1000, 100000, 0, 0)
     assert small > 0 and auto > 0
     assert lib.lw_spmv_workspace(0, 1000, 100000, 0, 0) == 0
+
+
+def test_hotx_entry_points_validate_without_a_device(lib):
+    """The hot-x packing entries reject bad shapes before touching a device."""
+    a = _lib.LwCsr()
+    a.rows, a.cols, a.nnz, a.offset_bits, a.dtype = 4, 4, 4, 32, _lib.LW_F32
+    n = ctypes.c_int32(0)
+    # slot cap above the one-CTA sort, negative cap, missing output count
+    assert lib.lw_hotx_build(ctypes.byref(a), 32769, None, None, ctypes.byref(n), None, 0, 0) \
+        == _lib.LW_E_INVALID_ARG
+    assert lib.lw_hotx_build(ctypes.byref(a), -1, None, None, ctypes.byref(n), None, 0, 0) \
+        == _lib.LW_E_INVALID_ARG
+    assert lib.lw_hotx_build(ctypes.byref(a), 16, None, None, None, None, 0, 0) == _lib.LW_E_INVALID_ARG
+    # packed SpMV: missing y / x, negative lanes
+    assert lib.lw_spmv_work_oriented_hotx(ctypes.byref(a), None, 0, None, None, 0, None, 0, 0) \
+        == _lib.LW_E_INVALID_ARG
+    # workspace grows with the hot slots and covers at least one slot
+    base = lib.lw_spmv_work_oriented_workspace(1000, 100000, 0, _lib.LW_F32)
+    w0 = lib.lw_spmv_work_oriented_hotx_workspace(1000, 100000, 0, 0, _lib.LW_F32)
+    w1 = lib.lw_spmv_work_oriented_hotx_workspace(1000, 100000, 0, 12288, _lib.LW_F32)
+    assert base < w0 < w1 and w1 - base >= 12288 * 4
+    assert lib.lw_hotx_build_workspace(1 << 20) >= (1 << 20) * 4
