@@ -558,8 +558,12 @@ static int traverse(const lw_csr_t* H, int64_t src, void* result, int schedule, 
     uint8_t* out = w.mask_out;
     const int64_t nb = scan_blocks(n);
     Pair* sums = (Pair*)w.sums;
-    int64_t* hc = nullptr;   // pinned (n_active, atoms) read back once per pass
-    LW_TRY(cudaMallocHost((void**)&hc, 16));
+    // pinned (n_active, atoms) read back once per pass: one 16-byte buffer per host
+    // thread, allocated on first use and kept (cudaFreeHost would synchronize the
+    // whole device on every call); a call completes before it returns, so the
+    // calls of one thread never share it concurrently
+    static thread_local int64_t* hc = nullptr;
+    if (!hc) LW_TRY(cudaHostAlloc((void**)&hc, 16, cudaHostAllocPortable));
     int rc = LW_OK;
     for (;;) {
         // one sweep: active[] = flatnonzero(in), fo[] = frontier edge offsets
@@ -591,7 +595,6 @@ static int traverse(const lw_csr_t* H, int64_t src, void* result, int schedule, 
         ++level;
         ++np;
     }
-    cudaFreeHost(hc);
     if (rc) return rc;
     if (passes) *passes = np;
     return LW_OK;

@@ -262,6 +262,32 @@ int lw_spmv(int schedule, const lw_csr_t* A, const void* x, void* y, int64_t lan
     }
 }
 
+// lw_spmv_host's device staging comes from a private stream-ordered pool per
+// device, created once and told to keep its freed memory mapped (re-mapping GBs
+// on every call would dominate it). Private, so the caller's default pool and
+// any other cudaMallocAsync user in the process keep their own release policy.
+static int staging_pool(cudaMemPool_t* out) {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
+    int dev = 0;
+    LW_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return LW_E_UNSUPPORTED;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!pools[dev]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t p;
+        LW_TRY(cudaMemPoolCreate(&p, &props));
+        uint64_t keep = UINT64_MAX;
+        LW_TRY(cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep));
+        pools[dev] = p;
+    }
+    *out = pools[dev];
+    return LW_OK;
+}
+
 int lw_spmv_host(int schedule, const lw_csr_t* H, const void* x_host, void* y_host, int64_t lanes,
                  int64_t gs, int64_t tpb, uintptr_t stream) {
     int rc = check_csr(H);
@@ -276,17 +302,9 @@ int lw_spmv_host(int schedule, const lw_csr_t* H, const void* x_host, void* y_ho
     auto up = [](size_t b) { return (b + 255) / 256 * 256; };
     const size_t bytes = up(off_b) + up(col_b) + up(val_b) + up(x_b) + up(y_b) + up(ws_b);
     unsigned char* d = nullptr;
-    {
-        // keep freed staging memory mapped in the default pool between calls (the
-        // pool otherwise unmaps it at every synchronize and re-maps GBs next call)
-        int dev = 0;
-        cudaMemPool_t pool;
-        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t keep = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-        }
-    }
-    LW_TRY(cudaMallocAsync((void**)&d, bytes > 0 ? bytes : 256, s));
+    cudaMemPool_t pool;
+    if ((rc = staging_pool(&pool))) return rc;
+    LW_TRY(cudaMallocFromPoolAsync((void**)&d, bytes > 0 ? bytes : 256, pool, s));
     unsigned char* p = d;
     void* d_off = p; p += up(off_b);
     void* d_col = p; p += up(col_b);

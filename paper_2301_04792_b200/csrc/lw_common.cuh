@@ -97,56 +97,6 @@ __device__ __forceinline__ double ld_gather(const double* p) {
     return v;
 }
 
-// ---- mbarrier + TMA bulk copy (sm_90+/sm_100a) ---------------------------
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
-}
-__device__ __forceinline__ void fence_mbar_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        "selp.u32 %0, 1, 0, p;\n"
-        "}\n"
-        : "=r"(ok)
-        : "r"(smem_addr(bar)), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    while (!mbar_try_wait(bar, parity)) {
-    }
-}
-// 1-D bulk copy global -> shared, completing tx bytes on `bar`; evict-first in L2.
-// dst/src 16-byte aligned, bytes a multiple of 16.
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
-                                            uint64_t* bar, uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
-        "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
-        : "memory");
-}
-// named barrier over the first `threads` threads of the CTA
-__device__ __forceinline__ void bar_sync_named(int id, int threads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
-}
-
 // Row offsets are read a handful of times per row (search + staging): plain
 // read-only loads.
 template <class OffT>
@@ -167,22 +117,10 @@ __device__ __forceinline__ T shfl_up(T v, int d) {
     return __shfl_up_sync(0xffffffffu, v, d);
 }
 
-// Warp segmented suffix-reduction over keys that are nondecreasing across lanes:
-// afterwards the first lane of every key run holds the run's sum.
-__device__ __forceinline__ double warp_segsum_to_head(double v, int key, int lane) {
-#pragma unroll
-    for (int d = 1; d < kWarp; d <<= 1) {
-        double ov = shfl_down(v, d);
-        int ok = shfl_down(key, d);
-        if (lane + d < kWarp && ok == key) v += ov;
-    }
-    return v;
-}
-
-// Same result shape from a ballot of segment heads (keys nondecreasing across
-// lanes, head = first lane of a run): each level moves one value (one SHFL for
-// fp32 partials, two for fp64) instead of the value and the key, and the run
-// boundary comes from the head mask instead of key compares.
+// Warp segmented suffix-reduction from a ballot of segment heads (keys
+// nondecreasing across lanes, head = first lane of a run): afterwards the head
+// lane of every run holds the run's sum. Each level moves one value (one SHFL
+// for fp32 partials, two for fp64); run boundaries come from the head mask.
 template <class R>
 __device__ __forceinline__ R warp_segsum_heads(R v, int lane, uint32_t heads) {
     // last lane of my run: the lane before the next head above me (or 31)

@@ -68,6 +68,39 @@ class DeviceCsr:
     col_indices: "object"   # torch int32 [nnz]
     values: "object"        # torch float32/float64 [nnz]
 
+    def __post_init__(self):
+        self._check()
+
+    def _check(self) -> None:
+        """The layout the kernels assume (lw_csr_t, include/lw_b200.h): raises
+        ValueError instead of letting a kernel read a wrongly typed, strided or
+        short array."""
+        torch = _torch()
+        off, col, val = self.row_offsets, self.col_indices, self.values
+        for name, t in (("row_offsets", off), ("col_indices", col), ("values", val)):
+            if not isinstance(t, torch.Tensor):
+                raise TypeError(f"DeviceCsr.{name} must be a torch tensor")
+            if t.ndim != 1 or not t.is_contiguous():
+                raise ValueError(f"DeviceCsr.{name} must be a contiguous 1-D tensor")
+            if t.device.type != "cuda":
+                raise ValueError(f"DeviceCsr.{name} must live on a CUDA device")
+        if not (off.device == col.device == val.device):
+            raise ValueError("DeviceCsr tensors must share one CUDA device")
+        if col.dtype != torch.int32:
+            raise ValueError(f"col_indices must be int32, got {col.dtype}")
+        if off.dtype not in (torch.int32, torch.int64):
+            raise ValueError(f"row_offsets must be int32 or int64, got {off.dtype}")
+        if val.dtype not in (torch.float32, torch.float64):
+            raise ValueError(f"values must be float32 or float64, got {val.dtype}")
+        if self.rows < 0 or self.cols < 0 or self.cols >= (1 << 31):
+            raise ValueError("rows must be >= 0 and 0 <= cols < 2^31")
+        if off.shape[0] != self.rows + 1:
+            raise ValueError(f"row_offsets has {off.shape[0]} entries, expected rows+1 = {self.rows + 1}")
+        if val.shape[0] != col.shape[0]:
+            raise ValueError("values and col_indices differ in length")
+        if off.dtype == torch.int32 and col.shape[0] >= (1 << 31):
+            raise ValueError("nnz >= 2^31 needs int64 row_offsets")
+
     @property
     def nnz(self) -> int:
         return int(self.col_indices.shape[0])
@@ -139,11 +172,14 @@ class DeviceCsr:
                          self.col_indices[a0:a1], self.values[a0:a1])
 
     def c_struct(self) -> _lib.LwCsr:
-        """The lw_csr_t view (cached while the three tensors are the same objects)."""
-        key = (id(self.row_offsets), id(self.col_indices), id(self.values), self.rows, self.cols)
+        """The lw_csr_t view, cached while the three tensors are the same objects
+        (held strongly, compared with ``is``) at the same ``_version`` (in-place
+        edits bump it)."""
+        key = self._tensor_key()
         hit = self.__dict__.get("_c_struct")
-        if hit is not None and hit[0] == key:
+        if hit is not None and _same_key(hit[0], key):
             return hit[1]
+        self._check()
         s = self._make_c_struct()
         self.__dict__["_c_struct"] = (key, s)
         return s
@@ -195,13 +231,21 @@ class DeviceCsr:
     def hot_columns(self) -> "HotColumns | None":
         """The hot-x packing built by pack_hot_columns, if the tensors are unchanged."""
         hx = self.__dict__.get("_hotx")
-        return hx if hx is not None and hx.key == self._tensor_key() else None
+        if hx is None:
+            return None
+        if not _same_key(hx.key, self._tensor_key()):
+            self.__dict__.pop("_hotx", None)   # the source tensors changed: drop the packing
+            return None
+        return hx
 
     def drop_hot_columns(self) -> None:
         self.__dict__.pop("_hotx", None)
 
     def _tensor_key(self):
-        return (id(self.row_offsets), id(self.col_indices), id(self.values), self.rows, self.cols)
+        """Strong references to the three tensors plus their versions: a cache
+        entry matches only the very same tensor objects, unmodified."""
+        ts = (self.row_offsets, self.col_indices, self.values)
+        return (ts, tuple(t._version for t in ts), self.rows, self.cols)
 
     def algorithmic_bytes(self) -> int:
         """SURVEY §8(d) byte model: nnz*(idx+val) + (rows+1)*off + cols*val + rows*val."""
@@ -216,21 +260,21 @@ def cached_device_csr(m, dtype="float64", device=None) -> "DeviceCsr":
     The reference's containers are immutable by convention (reference
     sparse.py:1-7), so a host-API call (``spmv(m, x)`` with NumPy operands) need
     not re-upload the matrix every time: the DeviceCsr is kept on the matrix and
-    reused while ``rows``, ``cols`` and the three arrays (identity, address,
-    length) are unchanged. Rebinding an array (``m.values = ...``) re-uploads;
-    mutating one in place is outside the contract — call
-    ``drop_device_cache(m)`` after doing so.
+    reused while ``rows``, ``cols`` and the three arrays are unchanged. The cache
+    entry holds the arrays themselves and compares them with ``is`` (an id()
+    could be reused by a new array once the old one is freed), so rebinding an
+    array (``m.values = ...``) always re-uploads; mutating one in place is
+    outside the contract — call ``drop_device_cache(m)`` after doing so.
     """
     dev = _require_cuda(device)
     arrays = (m.row_offsets, m.col_indices, m.values)
-    key = (int(m.rows), int(m.cols), str(_torch_dtype(dtype)), str(dev),
-           tuple((id(a), a.ctypes.data, a.shape[0]) for a in arrays))
+    slot = (int(m.rows), int(m.cols), str(_torch_dtype(dtype)), str(dev))
     cache = m.__dict__.setdefault("_lw_device_cache", {})
-    hit = cache.get(key[:4])
-    if hit is not None and hit[0] == key:
+    hit = cache.get(slot)
+    if hit is not None and all(a is b for a, b in zip(hit[0], arrays)):
         return hit[1]
     d = DeviceCsr.from_host(m, dtype=dtype, device=dev)
-    cache[key[:4]] = (key, d)
+    cache[slot] = (arrays, d)
     return d
 
 
@@ -301,6 +345,11 @@ class HotColumns:
         hot = c < 0
         return torch.where(hot, self.hot_cols[(c & 0x7FFFFFFF).long().clamp_(max=max(self.n_hot - 1, 0))]
                            if self.n_hot else c, c)
+
+
+def _same_key(a, b) -> bool:
+    """Equality of two DeviceCsr._tensor_key() values: same tensor objects, same versions."""
+    return (all(x is y for x, y in zip(a[0], b[0])) and a[1] == b[1] and a[2:] == b[2:])
 
 
 def _offsets_tensor(ts, device):

@@ -232,28 +232,39 @@ def fixup_combine(carries, combine) -> None:
 
 
 class AtomicMinArray:
-    """Shared array of non-negative reals (or +inf) with atomic min (reference
-    executor.py:254-283). The device kernels do the same with atomicMin on the
-    fp64 bit pattern (csrc/frontier.cu), which orders like the values precisely
-    because they are non-negative; host code gets this lock-based twin."""
+    """Slots of non-negative reals (or +inf) with an atomic min — the host twin
+    of the device kernels' relaxation (csrc/frontier.cu), built the same way:
+    a non-negative double orders exactly like its 64-bit pattern read as a
+    signed integer, so the min is an integer compare-and-store on the bits.
+    Python has no CAS, so each store runs under one of a fixed set of striped
+    locks (slot i uses lock i % STRIPES): updates of one slot are serialised,
+    updates of different slots mostly are not. Negative values are rejected
+    (their bit patterns would order backwards), as in reference
+    executor.py:254-283."""
+
+    STRIPES = 64
 
     def __init__(self, values: np.ndarray):
-        self.values = np.asarray(values, dtype=np.float64)
-        if self.values.size and np.nanmin(self.values) < 0:
+        vals = np.asarray(values, dtype=np.float64)
+        if vals.size and bool((vals < 0).any()):
             raise ValueError("slots must hold non-negative reals or +inf")
-        self._lock = threading.Lock()
+        self.values = vals
+        self._bits = vals.view(np.int64)
+        self._locks = tuple(threading.Lock() for _ in range(self.STRIPES))
 
     def atomic_min(self, index: int, candidate: float) -> float:
-        """Set slot ``index`` to min(slot, candidate); returns the prior value."""
-        if not candidate >= 0:
+        """Lower slot ``index`` to ``candidate`` if smaller; returns the prior value."""
+        c = float(candidate)
+        if not c >= 0.0:
             raise ValueError("candidate must be non-negative")
-        with self._lock:
-            previous = float(self.values[index])
-            if candidate < previous:
-                self.values[index] = candidate
-            return previous
+        bits = int(np.float64(c + 0.0).view(np.int64))   # + 0.0 folds -0.0 into +0.0
+        with self._locks[index % self.STRIPES]:
+            prior = int(self._bits[index])
+            if bits < prior:
+                self._bits[index] = bits
+        return float(np.int64(prior).view(np.float64))
 
 
 def atomic_min_real(slots: AtomicMinArray, index: int, candidate: float) -> float:
-    """Function-call spelling of :meth:`AtomicMinArray.atomic_min`."""
+    """Function form of :meth:`AtomicMinArray.atomic_min`."""
     return slots.atomic_min(index, candidate)

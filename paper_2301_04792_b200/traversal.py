@@ -38,10 +38,21 @@ _WS = Workspace()
 
 
 def device_graph(g, dtype="float64") -> DeviceCsr:
-    """A Graph (host) uploaded as a square DeviceCsr, or a DeviceCsr checked square."""
+    """A Graph (host) uploaded as a square DeviceCsr, or a DeviceCsr checked the
+    way reference Graph checks a host matrix (sparse.py:114-118): square, and no
+    negative edge weight (the SSSP kernels' atomicMin on the fp64 bit pattern is
+    only an order-preserving min for non-negative values). The weight check is
+    one device reduction per values tensor, remembered while that tensor is the
+    same object at the same version."""
     if isinstance(g, DeviceCsr):
         if g.rows != g.cols:
             raise ValueError("adjacency matrix must be square")
+        v = g.values
+        seen = g.__dict__.get("_nonneg_checked")
+        if seen is None or seen[0] is not v or seen[1] != v._version:
+            if g.nnz and bool((v < 0).any().item()):
+                raise ValueError("edge weights must be non-negative")
+            g.__dict__["_nonneg_checked"] = (v, v._version)
         return g
     if not isinstance(g, Graph):
         g = Graph(g)
