@@ -78,6 +78,11 @@ def parse():
                          "chunk's SpMV (0 = 4 when N > 1, else 1)")
     ap.add_argument("--items", type=int, default=0,
                     help="work_oriented items per lane (0 = library default)")
+    ap.add_argument("--no-fp64", action="store_true", help="skip the fp64 C3 leg")
+    ap.add_argument("--no-power", action="store_true", help="skip the C5 power-iteration leg")
+    ap.add_argument("--power-scale", type=int, default=26, help="R-MAT scale of the C5 leg")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch path only: rendezvous + one gloo all-reduce, no device work")
     return ap.parse_args()
 
 
@@ -206,7 +211,7 @@ def reference_arm(args):
         t = time.perf_counter()
         step()
         times.append(time.perf_counter() - t)
-    sec = float(np.mean(times))
+    sec = float(np.mean(times))     # whole job: K steps / their total time
     gflops = 2.0 * nnz * iters / sec / 1e9
     sample = (f"full R-MAT scale {args.scale} matrix ({rows} rows, {nnz} nnz), merge-path, "
               f"fp64/int64, {threads} threads, {lanes} lanes, mean of {args.steps} runs")
@@ -215,33 +220,78 @@ def reference_arm(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"rmat{args.scale}-ef{args.edge_factor}-seed{args.seed}",
-                   "schedule": "merge-path", "rows": rows, "nnz": nnz},
+        "config": run_config(args, rows, nnz, 1),
         "cpu_baseline": {"value": round(gflops, 4), "unit": "GFLOP/s", "cores": threads,
-                         "kind": "port", "sample": sample},
+                         "kind": "port", "sample": sample, "host": host_cpu(),
+                         "median_ms": round(float(np.median(times)) * 1e3, 3)},
         "e2e": {"value": round(gflops, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "generation_s": round(gen_s, 2),
     }
+    if args.mode != "power":
+        line["reference_package"] = time_lanework(off, col, val, x, threads)
     print(json.dumps(line), flush=True)
 
 
+def time_lanework(off, col, val, x, threads) -> dict:
+    """lanework itself (baseline/_ref, installed offline from the reference's
+    source; numba backend) on the same arrays: lanework.spmv(m, x,
+    ExecutorConfig(merge-path, worker_threads=all)) — the reference CLI's call —
+    warm-up (JIT) then the median of 5 (cli.py:137-145). Reported beside the
+    port, which is faster than lanework here, so the ratios the
+    driver computes against the port understate the speed-up over the reference."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "lanework").is_dir():
+        return {"unavailable": "baseline/_ref/lanework not installed"}
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/lw_numba_cache")
+    sys.path.insert(0, str(ref))
+    try:
+        import lanework
+    except Exception as exc:  # pragma: no cover - depends on the box
+        return {"unavailable": f"import failed: {exc!r}"}
+    finally:
+        sys.path.remove(str(ref))
+    try:
+        rows = off.size - 1
+        m = lanework.CsrMatrix(rows, rows, off, col, val)
+        cfg = lanework.ExecutorConfig(schedule=lanework.ScheduleKind.MERGE_PATH,
+                                      worker_threads=threads)
+        t = time.perf_counter()
+        lanework.spmv(m, x, cfg)
+        first = time.perf_counter() - t
+        ts = []
+        for _ in range(5):
+            t = time.perf_counter()
+            lanework.spmv(m, x, cfg)
+            ts.append(time.perf_counter() - t)
+        sec = float(np.median(ts))
+        return {"value": round(2.0 * int(off[-1]) / sec / 1e9, 4), "unit": "GFLOP/s",
+                "ms_per_step": round(sec * 1e3, 2), "first_call_ms": round(first * 1e3, 1),
+                "backend": lanework.backend_name(), "worker_threads": threads, "lanes": cfg.lanes,
+                "sample": "lanework.spmv on the full matrix, median of 5 after one warm-up call"}
+    except Exception as exc:  # pragma: no cover
+        return {"unavailable": f"lanework.spmv failed: {exc!r}"}
+
+
+def run_config(args, rows, nnz, world) -> dict:
+    """The workload description both arms share (same keys, same values)."""
+    return {"workload": f"rmat{args.scale}-ef{args.edge_factor}-seed{args.seed}",
+            "schedule": args.schedule, "rows": rows, "nnz": nnz,
+            "parallelism": f"rows{world}" if world > 1 else "single"}
+
+
 # ---------------------------------------------------------------------------------------
-def power_arm(args):
-    """C5: x <- A x / ||A x|| for --iters iterations on nnz-balanced row shards.
-    One step = the whole iteration sequence; each iteration is the shard's
-    work_oriented SpMV plus one NCCL all-gather of the uneven y shards."""
+def setup_ranks():
+    """(world, rank, local, dev) with the process group initialised for N > 1:
+    NCCL over NVLink, one rank per GPU. LW_BENCH_SHARE_GPU=1 (code-path check
+    only, never a measurement) puts every rank on cuda:0 over gloo, so the N > 1
+    path runs on a one-GPU box."""
     import torch
     import torch.distributed as dist
-
-    import paper_2301_04792_b200 as lwb
-    from paper_2301_04792_b200.distributed import RowShard, nnz_balanced_bounds, power_iteration
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    # LW_BENCH_SHARE_GPU=1 (code-path check only, never a measurement): every
-    # rank on cuda:0 over gloo, so the N > 1 path runs on a one-GPU box
     share = os.environ.get("LW_BENCH_SHARE_GPU") == "1"
     local = 0 if share else local
     torch.cuda.set_device(local)
@@ -251,8 +301,35 @@ def power_arm(args):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=dev)
+    return world, rank, local, dev
+
+
+def power_arm(args):
+    """--mode power: the C5 line alone (see power_measure)."""
+    import torch.distributed as dist
+
+    world, rank, local, dev = setup_ranks()
+    line = power_measure(args, world, rank, local, dev, args.scale, args.seed)
+    if world > 1:
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def power_measure(args, world, rank, local, dev, scale, seed):
+    """C5: x <- A x / ||A x|| for --iters iterations on nnz-balanced row shards.
+    One step = the whole iteration sequence; each iteration is the shard's
+    work_oriented SpMV plus one NCCL all-gather of the uneven y shards (row
+    chunks whose all-gathers overlap the next chunk's SpMV when N > 1), or with
+    --fused the all-gather folded into the SpMV's row stores. Returns the line."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2301_04792_b200 as lwb
+    from paper_2301_04792_b200.distributed import RowShard, nnz_balanced_bounds, power_iteration
+
     dtype = "float32" if args.dtype == "fp32" else "float64"
-    full = lwb.generate_rmat_csr(args.scale, args.edge_factor, args.seed, dtype=dtype, device=dev)
+    full = lwb.generate_rmat_csr(scale, args.edge_factor, seed, dtype=dtype, device=dev)
     n, nnz_total = full.rows, full.nnz
     bounds = nnz_balanced_bounds(full.row_offsets.cpu().numpy(), world)
     shard = RowShard(bounds, rank)
@@ -339,7 +416,7 @@ def power_arm(args):
         "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32" if args.dtype == "fp32" else "f64",
         "data": "synthetic",
-        "config": {"workload": f"rmat{args.scale}-ef{args.edge_factor}-seed{args.seed}-power{args.iters}",
+        "config": {"workload": f"rmat{scale}-ef{args.edge_factor}-seed{seed}-power{args.iters}",
                    "rows": n, "nnz": nnz_total, "parallelism": f"rows{world}" if world > 1 else "single",
                    "overlap_chunks": 0 if (args.fused or args.graph) else chunks,
                    "fused_allgather": bool(args.fused), "cuda_graph": bool(args.graph),
@@ -351,10 +428,9 @@ def power_arm(args):
                         * args.iters * args.steps,
         "clocks": clocks.summary(),
     }
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    del A, pieces
+    torch.cuda.empty_cache()
+    return line
 
 
 # ---------------------------------------------------------------------------------------
@@ -367,20 +443,7 @@ def our_arm(args):
     from paper_2301_04792_b200.device import current_stream
     from paper_2301_04792_b200.distributed import nnz_balanced_bounds
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    # LW_BENCH_SHARE_GPU=1 (code-path check only, never a measurement): every
-    # rank on cuda:0 over gloo, so the N > 1 path runs on a one-GPU box
-    share = os.environ.get("LW_BENCH_SHARE_GPU") == "1"
-    local = 0 if share else local
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        if share:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=dev)
+    world, rank, local, dev = setup_ranks()
 
     def barrier():
         if world > 1:
@@ -537,10 +600,8 @@ def our_arm(args):
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32" if args.dtype == "fp32" else "f64", "data": "synthetic",
-        "config": {"workload": f"rmat{args.scale}-ef{args.edge_factor}-seed{args.seed}",
-                   "schedule": args.schedule, "rows": rows_total, "nnz": nnz_total,
-                   "parallelism": f"rows{world}" if world > 1 else "single",
-                   "l2": "inputs > L2 (2.2 GB matrix streamed per step); no flush"},
+        "config": run_config(args, rows_total, nnz_total, world),
+        "notes": {"l2": "inputs > L2 (2.2 GB matrix streamed per step); no flush"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
                      "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
                      "kernel": "k_wo_chunk" if sched is lwb.ScheduleKind.MERGE_PATH else args.schedule,
@@ -555,7 +616,7 @@ def our_arm(args):
         "clocks": clocks.summary(),
     }
     if hx is not None:
-        line["config"]["x_layout"] = (f"hot-x packed: {hx.n_hot} most gathered columns in a dense "
+        line["notes"]["x_layout"] = (f"hot-x packed: {hx.n_hot} most gathered columns in a dense "
                                       f"per-call copy kept in L1 (DESIGN.md 4e); one-time inspector "
                                       f"{hx_build_ms:.1f} ms outside the timed region")
         line["roofline"]["kernel"] = "k_wo_chunk (hot-x packed; the pack rides on the partition launch)"
@@ -586,12 +647,96 @@ def our_arm(args):
         line["e2e"] = e2e
         if world == 1:
             line["e2e_cold"] = e2e_host(A, args, lib, dev, nnz_total)
+    if hx is not None:
+        # one-time inspector vs per-call saving: SpMVs after which packing has paid
+        saved = ms_unpacked - ms
+        line["notes"]["hotx_break_even_spmvs"] = (round(hx_build_ms / saved, 1) if saved > 0
+                                                   else None)
+    if not args.no_fp64 and args.dtype == "fp32" and sched is lwb.ScheduleKind.MERGE_PATH:
+        line["fp64"] = fp64_leg(A, args, lib, dev, world, nnz_total, hbm)
+    if not args.no_e2e and world == 1 and sched is lwb.ScheduleKind.MERGE_PATH:
+        line["e2e_api"] = e2e_api(A, args, nnz_total)
     if not args.no_cpu_baseline and rank == 0 and world == 1:
         line["cpu_baseline"] = cpu_baseline(A, args)
-    if rank == 0:
-        print(json.dumps(line), flush=True)
+    if not args.no_power and args.mode == "spmv":
+        del A, x, y, ws
+        hx = None
+        torch.cuda.empty_cache()
+        barrier()
+        line["power"] = power_measure(args, world, rank, local, dev, args.power_scale, 5)
     if world > 1:
         dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def fp64_leg(A, args, lib, dev, world, nnz_total, hbm):
+    """The same C3 matrix with fp64 values (the reference's only precision,
+    sparse.py:55-58): work_oriented kernel, unpacked, timed like the headline."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2301_04792_b200 as lwb
+
+    A64 = A.astype("float64")
+    x = torch.ones(A64.cols, dtype=torch.float64, device=dev)
+    y = torch.empty(A64.rows, dtype=torch.float64, device=dev)
+    cfg = lwb.ExecutorConfig(schedule=lwb.ScheduleKind.MERGE_PATH)
+    for _ in range(max(args.warmup, 3)):
+        lwb.spmv(A64, x, cfg, out=y)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        lwb.spmv(A64, x, cfg, out=y)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    alg = A64.algorithmic_bytes()
+    out = {"dtype": "f64", "ms_per_step": round(ms, 4),
+           "value": round(2.0 * nnz_total / (ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
+           "hbm_gbs_step": round(alg / (ms * 1e-3) / 1e9, 1),
+           "frac_step": round(alg / (ms * 1e-3) / 1e9 / hbm, 4), "alg_bytes": alg,
+           "path": "lw_spmv_work_oriented (fp64 values and x, int32 columns), 3 launches per step"}
+    del A64, x, y
+    torch.cuda.empty_cache()
+    return out
+
+
+def e2e_api(A, args, nnz_total):
+    """The call a lanework user makes, unchanged: lw.spmv(CsrMatrix, ndarray)
+    with the reference's defaults (kernels.py:57-69: merge-path, fp64 arithmetic,
+    NumPy float64 x in and a new NumPy float64 y out). The CsrMatrix's device copy
+    is cached by the package after the first call (like numba's compiled kernel
+    in the reference); every timed call uploads x, runs the SpMV and returns y on
+    the host, timed by the wall clock around the synchronous call."""
+    import paper_2301_04792_b200 as lwb
+    from paper_2301_04792_b200.device import drop_device_cache
+
+    m = lwb.CsrMatrix(A.rows, A.cols, A.row_offsets.cpu().numpy().astype(np.int64),
+                      A.col_indices.cpu().numpy().astype(np.int64),
+                      A.values.cpu().numpy().astype(np.float64))
+    x = np.ones(A.cols)
+    for _ in range(3):
+        y = lwb.spmv(m, x)
+    ts = []
+    for _ in range(max(5, min(args.steps, 20))):
+        t = time.perf_counter()
+        y = lwb.spmv(m, x)
+        ts.append(time.perf_counter() - t)
+    sec = float(np.median(ts))
+    drop_device_cache(m)
+    return {"value": round(2.0 * nnz_total / sec / 1e9, 3), "unit": "GFLOP/s",
+            "ms_per_step": round(sec * 1e3, 3), "dtype": "f64", "steps": len(ts),
+            "h2d_bytes_per_step": int(x.nbytes), "d2h_bytes_per_step": int(y.nbytes),
+            "path": "paper_2301_04792_b200.spmv(CsrMatrix, numpy x) -> numpy y, default "
+                    "ExecutorConfig (merge-path), fp64; median wall time of the synchronous call"}
 
 
 def e2e_resident(A, args, lib, dev, nnz_total):
@@ -709,8 +854,25 @@ def e2e_host(A, args, lib, dev, nnz_total):
             "path": "lw_spmv_host (C ABI, pinned host CSR + x in, y out, stream-synchronized)"}
 
 
+def host_cpu() -> dict:
+    """The host the CPU legs ran on: lscpu model name, logical CPUs usable here."""
+    model = None
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    cpus = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    return {"model": model, "logical_cpus": cpus}
+
+
 def cpu_baseline(A, args):
-    """Reference CPU algorithm (oracle port of lanework merge-path, fp64) on the same matrix."""
+    """Reference CPU algorithm (oracle port of lanework merge-path, fp64) on the
+    same matrix, all host threads (lanes = 32 x threads, the reference CLI's
+    configuration) and 1 thread (32 lanes, the reference's default config);
+    median of --cpu-reps runs, the reference CLI's protocol (cli.py:137-145)."""
     from oracle import oracle
 
     threads = oracle.default_threads()
@@ -718,24 +880,91 @@ def cpu_baseline(A, args):
     col = A.col_indices.cpu().numpy().astype(np.int64)
     val = A.values.cpu().numpy().astype(np.float64)
     x = np.ones(A.cols)
-    lanes = 32 * threads
-    oracle.spmv(off, col, val, x, "merge-path", lanes=lanes, threads=threads)
-    times = []
-    for _ in range(args.cpu_reps):
-        t = time.perf_counter()
-        oracle.spmv(off, col, val, x, "merge-path", lanes=lanes, threads=threads)
-        times.append(time.perf_counter() - t)
-    sec = float(np.median(times))
+
+    def med(th, reps):
+        oracle.spmv(off, col, val, x, "merge-path", lanes=32 * th, threads=th)
+        ts = []
+        for _ in range(reps):
+            t = time.perf_counter()
+            oracle.spmv(off, col, val, x, "merge-path", lanes=32 * th, threads=th)
+            ts.append(time.perf_counter() - t)
+        return float(np.median(ts))
+
+    sec = med(threads, max(args.cpu_reps, 3))
+    sec1 = med(1, 1)
     return {"value": round(2.0 * A.nnz / sec / 1e9, 4), "unit": "GFLOP/s", "cores": threads,
             "kind": "port", "ms_per_step": round(sec * 1e3, 2),
+            "one_thread": {"value": round(2.0 * A.nnz / sec1 / 1e9, 4), "ms_per_step": round(sec1 * 1e3, 1),
+                           "lanes": 32},
+            "host": host_cpu(),
             "sample": (f"full matrix ({A.rows} rows, {A.nnz} nnz), oracle port of lanework "
-                       f"merge-path (fp64/int64), {lanes} lanes on {threads} threads, median of "
-                       f"{args.cpu_reps}")}
+                       f"merge-path (fp64/int64), {32 * threads} lanes on {threads} threads, median of "
+                       f"{max(args.cpu_reps, 3)}; one_thread: 32 lanes on 1 thread, 1 run")}
+
+
+def _free_port() -> int:
+    import socket
+
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(args) -> int | None:
+    """`python bench.py --gpus N` (N > 1) outside torchrun re-executes itself
+    under torch.distributed.run with N ranks on this node (127.0.0.1
+    rendezvous), so the driver's plain command and its torchrun form give the
+    same N-rank run. NCCL's INIT log stays on (the driver counts ranks from it);
+    rank 0 prints the JSON line after the communicators are destroyed, so it is
+    the last line of stdout. Returns the child's exit code, or None when this
+    process is already a rank (or N == 1, or the reference arm: rank 0 only)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.impl == "reference":
+        return None
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("OMP_NUM_THREADS", "1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={_free_port()}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
+def check_world(args) -> None:
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl != "reference" and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} "
+                         f"(launch with --nproc-per-node {args.gpus}, or without torchrun)")
+
+
+def dry_run(args) -> None:
+    """--dry-run: the launch path alone (rendezvous, one all-reduce over gloo,
+    the rank count on rank 0's line) — no device work; CPU-testable."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    seen = world
+    if world > 1:
+        dist.init_process_group("gloo")
+        t = torch.ones(1)
+        dist.all_reduce(t)
+        seen = int(t.item())
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks_in_allreduce": seen}), flush=True)
 
 
 def main():
     args = parse()
-    if args.impl == "reference":
+    rc = self_launch(args)
+    if rc is not None:
+        sys.exit(rc)
+    check_world(args)
+    if args.dry_run:
+        dry_run(args)
+    elif args.impl == "reference":
         reference_arm(args)
     elif args.mode == "power":
         power_arm(args)

@@ -316,6 +316,13 @@ int lw_coo_to_csr_host(int64_t rows, int64_t cols, int64_t n, const int64_t* row
 int lw_rmat_keys(int32_t scale, int64_t edge_begin, int64_t n_edges, uint32_t t_a, uint32_t t_ab,
                  uint32_t t_abc, uint64_t seed, int64_t* keys, uintptr_t stream);
 
+/* Uniform keys: keys[i] = lw_uniform_key(seed, begin + i, space) in [0, space)
+ * (row * cols + col for a rows x cols matrix; sorted + deduplicated by the
+ * caller). Feeds the uniform-random configs (C2u, C4 uniform) at sizes the
+ * reference's host generator (sparse.py:164-187) takes minutes to build. */
+int lw_uniform_keys(int64_t space, int64_t begin, int64_t n, uint64_t seed, int64_t* keys,
+                    uintptr_t stream);
+
 /* values[i] = U[-1,1) drawn from hash(seed, key[i]); dtype LW_F32 rounds the fp64
  * draw to fp32. */
 int lw_hash_values(const int64_t* keys, int64_t n, uint64_t seed, int32_t dtype,

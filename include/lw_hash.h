@@ -52,6 +52,17 @@ LW_HD uint64_t lw_rmat_key(uint64_t seed, uint64_t edge, int scale, uint32_t t_a
     return (row << scale) | col;
 }
 
+/* Uniform position in [0, space) of draw i (the C2u / C4-uniform generator):
+ * the high 64 bits of a 64x64-bit product of the draw's root with space. */
+LW_HD uint64_t lw_uniform_key(uint64_t seed, uint64_t i, uint64_t space) {
+    const uint64_t r = lw_edge_root(seed ^ 0x2545F4914F6CDD1DULL, i);
+#ifdef __CUDA_ARCH__
+    return __umul64hi(r, space);
+#else
+    return (uint64_t)(((unsigned __int128)r * space) >> 64);
+#endif
+}
+
 /* U[-1, 1) value keyed by a 64-bit position */
 LW_HD double lw_hash_value(uint64_t seed, uint64_t key) {
     uint64_t h = lw_mix64(lw_mix64(seed ^ 0x5851F42D4C957F2DULL) + key * LW_GOLDEN);

@@ -14,6 +14,7 @@
  * imports the reference and records partitions, plans, per-lane counts,
  * assignment maps and SpMV results; tests/test_oracle_golden.py replays them).
  */
+#include <math.h>
 #include <omp.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -367,6 +368,12 @@ EXPORT void lwo_rmat_keys(int scale, int64_t edge_begin, int64_t n_edges, uint32
         keys[i] = (int64_t)lw_rmat_key(seed, (uint64_t)(edge_begin + i), scale, ta, tab, tabc);
 }
 
+EXPORT void lwo_uniform_keys(int64_t space, int64_t begin, int64_t n, uint64_t seed, int64_t* keys,
+                             int threads) {
+#pragma omp parallel for num_threads(threads) schedule(static)
+    for (int64_t i = 0; i < n; ++i) keys[i] = (int64_t)lw_uniform_key(seed, (uint64_t)(begin + i), (uint64_t)space);
+}
+
 EXPORT void lwo_hash_values(const int64_t* keys, int64_t n, uint64_t seed, double* out,
                             int threads) {
 #pragma omp parallel for num_threads(threads) schedule(static)
@@ -440,3 +447,108 @@ EXPORT int64_t lwo_rmat_csr(int scale, int64_t edge_factor, uint32_t ta, uint32_
     free(tmp);
     return acc;
 }
+
+/* ---- full-size checks on the device layout ---------------------------------
+ * The same merge-path SpMV as lwo_spmv_merge_path (_fast.py:31-52 +
+ * kernels.py:80-91), reading the GPU's arrays as they come back from the device:
+ * offsets int32 or int64, columns int32, values and x float or double. Every
+ * element is widened on load to int64 / fp64 — the reference's own coercion
+ * (sparse.py:55-58, kernels.py:60) — so the arithmetic is the reference's, but a
+ * 1e9-atom matrix needs no 16 GB upcast copy. scale[r] = sum_j |A_rj x_j| (the
+ * north star's tolerance scale) comes out of the same pass, in the same lanes. */
+#define LWO_NARROW_SPMV(NAME, OFF_T, VAL_T)                                                     \
+    EXPORT int NAME(const OFF_T* off, const int32_t* col, const VAL_T* val, const VAL_T* x,      \
+                    double* y, double* scale, int64_t rows, int64_t lanes, int threads) {       \
+        const int64_t nnz = rows ? (int64_t)off[rows] : 0, total = rows + nnz;                  \
+        const int64_t items = total ? (total + lanes - 1) / lanes : 0;                          \
+        int64_t* coords = (int64_t*)malloc(sizeof(int64_t) * 2 * (size_t)(lanes + 1));          \
+        int64_t* ct = (int64_t*)malloc(sizeof(int64_t) * (size_t)lanes);                        \
+        double* cv = (double*)malloc(sizeof(double) * (size_t)lanes);                           \
+        double* cs = (double*)malloc(sizeof(double) * (size_t)lanes);                           \
+        if (!coords || !ct || !cv || !cs) {                                                      \
+            free(coords); free(ct); free(cv); free(cs);                                          \
+            return -1;                                                                           \
+        }                                                                                        \
+        _Pragma("omp parallel for num_threads(threads) schedule(static)")                        \
+        for (int64_t k = 0; k <= lanes; ++k) {                                                   \
+            const int64_t d = imin(k * items, total);                                            \
+            int64_t lo = imax(0, d - nnz), hi = imin(d, rows);                                   \
+            while (lo < hi) {                                                                    \
+                const int64_t mid = (lo + hi + 1) / 2;                                           \
+                if ((int64_t)off[mid] <= d - mid) lo = mid;                                      \
+                else hi = mid - 1;                                                               \
+            }                                                                                    \
+            coords[2 * k] = lo;                                                                  \
+            coords[2 * k + 1] = d - lo;                                                          \
+        }                                                                                        \
+        _Pragma("omp parallel for num_threads(threads) schedule(dynamic, 1)")                    \
+        for (int64_t lane = 0; lane < lanes; ++lane) {                                           \
+            int64_t atom = coords[2 * lane + 1];                                                 \
+            const int64_t tile_end = coords[2 * lane + 2], atom_end = coords[2 * lane + 3];      \
+            double acc = 0.0, sa = 0.0;                                                          \
+            for (int64_t t = coords[2 * lane]; t < tile_end; ++t) {                              \
+                for (; atom < (int64_t)off[t + 1]; ++atom) {                                     \
+                    const double p = (double)val[atom] * (double)x[col[atom]];                   \
+                    acc += p;                                                                    \
+                    sa += p < 0 ? -p : p;                                                        \
+                }                                                                                \
+                y[t] = acc;                                                                      \
+                scale[t] = sa;                                                                   \
+                acc = 0.0;                                                                       \
+                sa = 0.0;                                                                        \
+            }                                                                                    \
+            ct[lane] = -1;                                                                       \
+            cv[lane] = 0.0;                                                                      \
+            cs[lane] = 0.0;                                                                      \
+            if (atom < atom_end) {                                                               \
+                for (; atom < atom_end; ++atom) {                                                \
+                    const double p = (double)val[atom] * (double)x[col[atom]];                   \
+                    acc += p;                                                                    \
+                    sa += p < 0 ? -p : p;                                                        \
+                }                                                                                \
+                ct[lane] = tile_end;                                                             \
+                cv[lane] = acc;                                                                  \
+                cs[lane] = sa;                                                                   \
+            }                                                                                    \
+        }                                                                                        \
+        for (int64_t lane = 0; lane < lanes; ++lane)                                             \
+            if (ct[lane] >= 0) {                                                                 \
+                y[ct[lane]] += cv[lane];                                                         \
+                scale[ct[lane]] += cs[lane];                                                     \
+            }                                                                                    \
+        free(coords); free(ct); free(cv); free(cs);                                              \
+        return 0;                                                                                \
+    }
+
+LWO_NARROW_SPMV(lwo_spmv_narrow_o32_f32, int32_t, float)
+LWO_NARROW_SPMV(lwo_spmv_narrow_o32_f64, int32_t, double)
+LWO_NARROW_SPMV(lwo_spmv_narrow_o64_f32, int64_t, float)
+LWO_NARROW_SPMV(lwo_spmv_narrow_o64_f64, int64_t, double)
+
+/* max over rows of |y[r] - y_ref[r]| / (rtol * scale[r]) for a device result y
+ * (float or double): the north star's per-entry bound as one number (<= 1 passes).
+ * A row with scale 0 must match exactly (it holds only zero products). */
+#define LWO_TOL(NAME, Y_T)                                                                      \
+    EXPORT double NAME(const Y_T* y, const double* y_ref, const double* scale, int64_t rows,     \
+                       double rtol, int64_t* worst_row, int threads) {                          \
+        double worst = 0.0;                                                                      \
+        int64_t wr = -1;                                                                         \
+        _Pragma("omp parallel num_threads(threads)")                                             \
+        {                                                                                        \
+            double w = 0.0;                                                                      \
+            int64_t r0 = -1;                                                                     \
+            _Pragma("omp for schedule(static)")                                                  \
+            for (int64_t r = 0; r < rows; ++r) {                                                 \
+                const double e = fabs((double)y[r] - y_ref[r]);                                  \
+                const double q = scale[r] > 0 ? e / (rtol * scale[r]) : (e > 0 ? INFINITY : 0.0); \
+                if (q > w || q != q) { w = q != q ? INFINITY : q; r0 = r; }                      \
+            }                                                                                    \
+            _Pragma("omp critical")                                                              \
+            if (w > worst || (w == worst && r0 >= 0 && (wr < 0 || r0 < wr))) { worst = w; wr = r0; } \
+        }                                                                                        \
+        if (worst_row) *worst_row = wr;                                                          \
+        return worst;                                                                            \
+    }
+
+LWO_TOL(lwo_tolerance_f32, float)
+LWO_TOL(lwo_tolerance_f64, double)

@@ -69,8 +69,14 @@ def lib():
             "lwo_assign_group_mapped": (None, [_p, _i64, _i64, _i64, _i64, _p, _p, _p]),
             "lwo_rmat_keys": (None, [_int, _i64, _i64, _u32, _u32, _u32, _u64, _p, _int]),
             "lwo_hash_values": (None, [_p, _i64, _u64, _p, _int]),
+            "lwo_uniform_keys": (None, [_i64, _i64, _i64, _u64, _p, _int]),
             "lwo_rmat_csr": (_i64, [_int, _i64, _u32, _u32, _u32, _u64, _int, _p, _p, _p]),
+            "lwo_tolerance_f32": (ctypes.c_double, [_p, _p, _p, _i64, ctypes.c_double, _p, _int]),
+            "lwo_tolerance_f64": (ctypes.c_double, [_p, _p, _p, _i64, ctypes.c_double, _p, _int]),
         }
+        for ob in (32, 64):
+            for vb in (32, 64):
+                sig[f"lwo_spmv_narrow_o{ob}_f{vb}"] = (_int, [_p, _p, _p, _p, _p, _p, _i64, _i64, _int])
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
             fn.restype = res
@@ -230,6 +236,40 @@ def bfs(off, col, source: int) -> np.ndarray:
     return depth
 
 
+def spmv_narrow(off, col, val, x, lanes: int | None = None, threads: int | None = None):
+    """Merge-path y = A x (fp64 arithmetic, reference lanes + serial fix-up) on the
+    device layout as copied back from the GPU — offsets int32/int64, columns int32,
+    values and x float32/float64, widened element by element (lw_oracle.c
+    LWO_NARROW_SPMV). Returns (y_ref, scale) with scale = sum_j |A_ij x_j|."""
+    off = np.ascontiguousarray(off)
+    col = np.ascontiguousarray(col, dtype=np.int32)
+    val = np.ascontiguousarray(val)
+    if off.dtype not in (np.int32, np.int64) or val.dtype not in (np.float32, np.float64):
+        raise TypeError("offsets int32/int64, values float32/float64")
+    x = np.ascontiguousarray(x, dtype=val.dtype)
+    rows = off.size - 1
+    threads = threads or default_threads()
+    lanes = lanes or 32 * threads
+    y = np.empty(rows, dtype=np.float64)
+    scale = np.empty(rows, dtype=np.float64)
+    fn = getattr(lib(), f"lwo_spmv_narrow_o{off.itemsize * 8}_f{val.itemsize * 8}")
+    if fn(_ptr(off), _ptr(col), _ptr(val), _ptr(x), _ptr(y), _ptr(scale), rows, lanes, threads):
+        raise MemoryError("oracle narrow spmv allocation failed")
+    return y, scale
+
+
+def worst_ratio(y, y_ref, scale, rtol: float, threads: int | None = None) -> tuple[float, int]:
+    """max_r |y[r] - y_ref[r]| / (rtol * scale[r]) (<= 1 passes) and its row."""
+    y = np.ascontiguousarray(y)
+    if y.dtype not in (np.float32, np.float64):
+        y = y.astype(np.float64)
+    wr = ctypes.c_int64(-1)
+    fn = lib().lwo_tolerance_f32 if y.dtype == np.float32 else lib().lwo_tolerance_f64
+    w = fn(_ptr(y), _ptr(y_ref), _ptr(scale), y.size, rtol, ctypes.byref(wr),
+           threads or default_threads())
+    return float(w), int(wr.value)
+
+
 def abs_row_sums(off, col, val, x) -> np.ndarray:
     """sum_j |A_ij x_j| per row — the scale of the north star's tolerance."""
     off, col = _i64a(off), _i64a(col)
@@ -255,6 +295,19 @@ def rmat_keys(scale: int, n_edges: int, seed: int, thresholds, edge_begin: int =
     lib().lwo_rmat_keys(scale, edge_begin, n_edges, ta, tab, tabc, seed, _ptr(out),
                         threads or default_threads())
     return out
+
+
+def uniform_csr(rows: int, cols: int, nnz_target: int, seed: int, threads: int | None = None):
+    """Host twin of device.generate_uniform_device: (off, col, val) int64/int64/fp64."""
+    keys = np.empty(nnz_target, dtype=np.int64)
+    lib().lwo_uniform_keys(rows * cols, 0, nnz_target, seed, _ptr(keys), threads or default_threads())
+    keys = np.unique(keys)
+    val = np.empty(keys.size, dtype=np.float64)
+    lib().lwo_hash_values(_ptr(keys), keys.size, seed, _ptr(val), threads or default_threads())
+    r = keys // cols
+    off = np.zeros(rows + 1, dtype=np.int64)
+    np.cumsum(np.bincount(r, minlength=rows), out=off[1:])
+    return off, keys - r * cols, val
 
 
 def rmat_csr(scale: int, edge_factor: int, seed: int, thresholds, threads: int | None = None):

@@ -12,7 +12,8 @@ from ._backend import (ENV_VAR, NUMBA_AVAILABLE, backend_name, cuda_active, cuda
                        numba_active, use_backend)
 from ._lib import BackendUnavailable
 from .device import (DeviceCsr, HotColumns, device_group_plan_prefix, device_merge_path_partition,
-                     generate_banded_device, generate_rmat_csr)
+                     generate_banded_device, generate_rmat_csr,
+                     generate_uniform_device)
 from .executor import (SENTINEL_TILE, SUM_CARRIES, AtomicMinArray, CarryOut, CarryPolicy,
                        ExecutorConfig, ImbalanceReport, atomic_min_real, device_config,
                        execute_merge_path, execute_tile_major, fixup_combine, imbalance)
@@ -49,7 +50,7 @@ __all__ = [
     "device_group_plan_prefix", "device_merge_path_partition", "exclusive_prefix_sum",
     "execute_merge_path", "execute_tile_major", "fixup_combine", "generate_banded_csr",
     "generate_banded_device", "generate_power_law_csr", "generate_random_csr",
-    "generate_rmat_csr", "get_tile", "group_plan", "imbalance", "infinite_range",
+    "generate_rmat_csr", "generate_uniform_device", "get_tile", "group_plan", "imbalance", "infinite_range",
     "lane_stride_range", "make_schedule", "merge_path_partition", "merge_path_search",
     "merge_path_slices", "num_blocks", "numba_active", "rmat_thresholds", "row_length_stats",
     "spmm", "spmv", "spmv_auto", "spmv_probe", "step_range", "thread_mapped_tiles", "tile_offsets",

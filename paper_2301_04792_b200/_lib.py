@@ -71,6 +71,7 @@ EXPORTS = (
     "lw_coo_to_csr_host",
     "lw_rmat_keys",
     "lw_hash_values",
+    "lw_uniform_keys",
 )
 
 
@@ -180,6 +181,7 @@ _SIGNATURES = {
                                           ctypes.POINTER(_i64), _i32]),
     "lw_rmat_keys": (ctypes.c_int, [_i32, _i64, _i64, _u32, _u32, _u32, _u64, _vp, _up]),
     "lw_hash_values": (ctypes.c_int, [_vp, _i64, _u64, _i32, _vp, _up]),
+    "lw_uniform_keys": (ctypes.c_int, [_i64, _i64, _i64, _u64, _vp, _up]),
 }
 
 

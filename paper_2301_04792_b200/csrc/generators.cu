@@ -19,6 +19,13 @@ __global__ void k_rmat_keys(int scale, int64_t edge_begin, int64_t n_edges, uint
         keys[i] = (int64_t)lw_rmat_key(seed, (uint64_t)(edge_begin + i), scale, t_a, t_ab, t_abc);
 }
 
+__global__ void k_uniform_keys(uint64_t space, int64_t begin, int64_t n, uint64_t seed,
+                               int64_t* __restrict__ keys) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        keys[i] = (int64_t)lw_uniform_key(seed, (uint64_t)(begin + i), space);
+}
+
 template <class ValT>
 __global__ void k_hash_values(const int64_t* __restrict__ keys, int64_t n, uint64_t seed,
                               ValT* __restrict__ out) {
@@ -34,6 +41,15 @@ int rmat_keys(int scale, int64_t edge_begin, int64_t n_edges, uint32_t t_a, uint
     if (n_edges == 0) return LW_OK;
     const int64_t grid = min(ceil_div(n_edges, 256), (int64_t)sm_count() * 16);
     k_rmat_keys<<<grid, 256, 0, s>>>(scale, edge_begin, n_edges, t_a, t_ab, t_abc, seed, keys);
+    LW_LAUNCH_CHECK();
+    return LW_OK;
+}
+
+int uniform_keys(int64_t space, int64_t begin, int64_t n, uint64_t seed, int64_t* keys, cudaStream_t s) {
+    if (space < 1 || n < 0 || begin < 0 || (!keys && n > 0)) return LW_E_INVALID_ARG;
+    if (n == 0) return LW_OK;
+    const int64_t grid = min(ceil_div(n, 256), (int64_t)sm_count() * 16);
+    k_uniform_keys<<<grid, 256, 0, s>>>((uint64_t)space, begin, n, seed, keys);
     LW_LAUNCH_CHECK();
     return LW_OK;
 }

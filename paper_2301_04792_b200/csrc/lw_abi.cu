@@ -17,6 +17,7 @@ int merge_path_partition(int64_t, int64_t, const void*, int, int64_t, int64_t*, 
 int group_plan_prefix(int64_t, const void*, int, int64_t, int64_t*, cudaStream_t);
 int rmat_keys(int, int64_t, int64_t, uint32_t, uint32_t, uint32_t, uint64_t, int64_t*, cudaStream_t);
 int hash_values(const int64_t*, int64_t, uint64_t, int, void*, cudaStream_t);
+int uniform_keys(int64_t, int64_t, int64_t, uint64_t, int64_t*, cudaStream_t);
 int spmm(int, const lw_csr_t*, const void*, void*, int64_t, int64_t, int64_t, int64_t, void*, size_t, cudaStream_t);
 int64_t spmm_auto_lanes(int schedule, int64_t rows, int64_t nnz, int64_t n, int64_t gs, int64_t tpb);
 size_t spmm_wo_workspace(int64_t lanes, int64_t n);
@@ -478,6 +479,11 @@ int lw_bfs(const lw_csr_t* G, int64_t source, int64_t* depth, int schedule, int6
 int lw_rmat_keys(int32_t scale, int64_t edge_begin, int64_t n_edges, uint32_t t_a, uint32_t t_ab,
                  uint32_t t_abc, uint64_t seed, int64_t* keys, uintptr_t stream) {
     return rmat_keys(scale, edge_begin, n_edges, t_a, t_ab, t_abc, seed, keys, (cudaStream_t)stream);
+}
+
+int lw_uniform_keys(int64_t space, int64_t begin, int64_t n, uint64_t seed, int64_t* keys,
+                    uintptr_t stream) {
+    return uniform_keys(space, begin, n, seed, keys, (cudaStream_t)stream);
 }
 
 int lw_hash_values(const int64_t* keys, int64_t n, uint64_t seed, int32_t dtype, void* values,

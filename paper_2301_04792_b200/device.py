@@ -436,6 +436,47 @@ def generate_rmat_csr(scale: int, edge_factor: int = 16, seed: int = 3, a: float
     return _csr_from_sorted_keys(n, scale, keys, seed, dtype, dev)
 
 
+def generate_uniform_device(rows: int, cols: int, nnz_target: int, seed: int, dtype="float32",
+                            device=None, chunk: int = 1 << 27) -> DeviceCsr:
+    """Uniform-random rows x cols CSR built on the device (the C2u / C4-uniform
+    inputs): nnz_target positions drawn uniformly from [0, rows*cols) with
+    lw_uniform_key, duplicates removed (so nnz <= nnz_target, short by about
+    nnz^2 / (2 rows cols)), values hash_values(row*cols + col, seed) in U[-1, 1).
+    The reference's own generate_random_csr (sparse.py:164-187) draws exactly
+    nnz_target distinct positions with NumPy and takes minutes at 32M atoms; the
+    oracle's lwo_uniform_keys evaluates the same key function on the host."""
+    torch = _torch()
+    dev = _require_cuda(device)
+    if rows < 1 or cols < 1 or nnz_target < 0:
+        raise ValueError("rows, cols must be positive and nnz_target non-negative")
+    space = rows * cols
+    lib = _lib.load()
+    stream = current_stream(dev)
+    uniq = []
+    for start in range(0, nnz_target, chunk):
+        cnt = min(chunk, nnz_target - start)
+        k = torch.empty(cnt, dtype=torch.int64, device=dev)
+        _lib.check(lib.lw_uniform_keys(space, start, cnt, seed, k.data_ptr(), stream), "lw_uniform_keys")
+        uniq.append(torch.unique(k))
+        del k
+    if not uniq:
+        keys = torch.empty(0, dtype=torch.int64, device=dev)
+    else:
+        keys = torch.unique(torch.cat(uniq)) if len(uniq) > 1 else uniq[0]
+    del uniq
+    r = keys // cols
+    counts = torch.bincount(r, minlength=rows)
+    nnz = int(keys.shape[0])
+    off = torch.zeros(rows + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(counts, 0, out=off[1:])
+    vals = torch.empty(nnz, dtype=_torch_dtype(dtype), device=dev)
+    if nnz:
+        _lib.check(lib.lw_hash_values(keys.data_ptr(), nnz, seed, _dtype_code(dtype), vals.data_ptr(),
+                                      stream), "lw_hash_values")
+    odt = torch.int32 if nnz < (1 << 31) else torch.int64
+    return DeviceCsr(rows, cols, off.to(odt), (keys - r * cols).to(torch.int32), vals)
+
+
 def generate_banded_device(rows: int, half_bandwidth: int, seed: int, dtype="float32",
                            device=None) -> DeviceCsr:
     """Banded matrix (sparse.generate_banded_csr) built directly on the device."""

@@ -1,14 +1,17 @@
 """Executor configuration, imbalance accounting and host schedule walkers.
 
-``ExecutorConfig`` keeps the reference's fields and validation
-(executor.py:35-72). One deliberate difference: ``lanes=None`` stays ``None``
-and means "sized for the device" — the cuda backend then picks P from the SM
-count (``lw_auto_lanes``) instead of the reference's ``worker_threads*32``,
-which would leave a B200 idle. Host-side helpers that need a number
-(``imbalance``, the walkers, ``group_count``) resolve ``None`` to
-``worker_threads*32`` exactly like the reference; ``device_config`` resolves it
-the way the kernels will, so ``imbalance(ts, device_config(cfg, m))`` predicts
-the per-thread atom counts of the actual launch.
+``ExecutorConfig`` keeps the reference's fields, defaults and validation
+(executor.py:35-72): ``lanes=None`` resolves to ``worker_threads*32`` in
+``__post_init__``, so reference code that reads ``cfg.lanes`` (or passes the
+config to ``imbalance`` and the walkers) sees exactly the reference's number.
+What the GPU launch does with it is recorded separately: a config built
+without an explicit ``lanes`` carries ``lanes_auto=True`` and the cuda backend
+then sizes P for the device (``lw_auto_lanes``, one resident wave of each
+kernel) instead of launching the reference's 32 CPU lanes, which would leave a
+B200 idle; an explicit ``lanes=P`` is launched as P lanes. ``device_config``
+returns the config with the launch's lane count filled in, so
+``imbalance(ts, device_config(cfg, m))`` predicts the per-thread atom counts of
+the actual launch.
 
 ``execute_tile_major`` / ``execute_merge_path`` / ``fixup_combine`` are the
 reference's callback API for custom per-atom work (executor.py:132-221). They
@@ -45,13 +48,19 @@ class ExecutorConfig:
     worker_threads: int = 1
     group_size: int = 32
     tiles_per_block: int | None = None
+    # True when lanes was not given: the device launch is sized for the GPU.
+    # Not an __init__ argument, so dataclasses.replace(cfg, lanes=P) is explicit.
+    lanes_auto: bool = field(default=False, init=False, repr=False, compare=False)
 
     def __post_init__(self):
         if not isinstance(self.schedule, ScheduleKind):
             self.schedule = ScheduleKind(self.schedule)
         if self.worker_threads < 1:
             raise ValueError("worker_threads must be >= 1")
-        if self.lanes is not None and self.lanes < 1:
+        if self.lanes is None:
+            self.lanes = self.worker_threads * 32
+            self.lanes_auto = True
+        if self.lanes < 1:
             raise ValueError("lanes must be >= 1")
         if self.group_size < 1:
             raise ValueError("group_size must be >= 1")
@@ -62,8 +71,8 @@ class ExecutorConfig:
 
     @property
     def lane_count(self) -> int:
-        """Lanes for host-side accounting: explicit lanes, else worker_threads*32."""
-        return self.lanes if self.lanes is not None else self.worker_threads * 32
+        """Lanes for host-side accounting (== lanes, the reference's P)."""
+        return self.lanes
 
     def group_lanes(self, group_id: int) -> range:
         lo = group_id * self.group_size
@@ -76,7 +85,7 @@ class ExecutorConfig:
 
 def device_config(cfg: ExecutorConfig, m) -> ExecutorConfig:
     """``cfg`` with ``lanes`` fixed to the value the device kernels will use for ``m``."""
-    if cfg.lanes is not None:
+    if not cfg.lanes_auto:
         return cfg
     from . import _lib
 

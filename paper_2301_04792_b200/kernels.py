@@ -10,8 +10,9 @@
   * device operands (DeviceCsr + torch CUDA x): y stays on the device in the
     matrix's dtype; nothing touches the host. This is the path the bench's
     ``value`` measures.
-Schedule selection follows ``cfg.schedule``; ``cfg.lanes=None`` lets the
-device size the lane count (see executor.device_config).
+Schedule selection follows ``cfg.schedule``; a config built without ``lanes``
+(``cfg.lanes_auto``) lets the device size the lane count (see
+executor.device_config); an explicit ``lanes=P`` launches P lanes.
 """
 
 from __future__ import annotations
@@ -39,7 +40,7 @@ def schedule_code(kind: ScheduleKind) -> int:
 
 
 def _lanes_arg(cfg: ExecutorConfig) -> int:
-    return 0 if cfg.lanes is None else int(cfg.lanes)
+    return 0 if cfg.lanes_auto else int(cfg.lanes)
 
 
 @functools.lru_cache(maxsize=256)

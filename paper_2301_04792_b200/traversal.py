@@ -65,7 +65,7 @@ def _ws(G: DeviceCsr):
 
 
 def _cfg_args(cfg: ExecutorConfig):
-    return (schedule_code(cfg.schedule), 0 if cfg.lanes is None else int(cfg.lanes),
+    return (schedule_code(cfg.schedule), 0 if cfg.lanes_auto else int(cfg.lanes),
             cfg.group_size, cfg.tiles_per_block)
 
 

@@ -144,9 +144,15 @@ def test_group_plan_get_tile_golden(golden):
 
 def test_executor_config_validation():
     c = lw.ExecutorConfig()
-    assert c.schedule is ScheduleKind.MERGE_PATH and c.lanes is None and c.lane_count == 32
+    # the reference resolves lanes=None to worker_threads*32 (executor.py:54-55)
+    assert c.schedule is ScheduleKind.MERGE_PATH and c.lanes == 32 and c.lane_count == 32
+    assert c.lanes_auto   # ... and the GPU launch is sized for the device
     assert c.tiles_per_block == 32 and c.group_count == 1
-    assert lw.ExecutorConfig(worker_threads=4).lane_count == 128
+    assert lw.ExecutorConfig(worker_threads=4).lanes == 128
+    explicit = lw.ExecutorConfig(lanes=32)
+    assert explicit.lanes == 32 and not explicit.lanes_auto
+    import dataclasses
+    assert not dataclasses.replace(c, lanes=64).lanes_auto
     assert lw.ExecutorConfig(schedule="work-oriented").schedule is ScheduleKind.MERGE_PATH
     for bad in (dict(worker_threads=0), dict(lanes=0), dict(group_size=0),
                 dict(tiles_per_block=0)):
