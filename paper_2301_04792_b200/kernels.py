@@ -23,7 +23,8 @@ from dataclasses import dataclass, replace
 import numpy as np
 
 from . import _backend, _lib
-from .device import DeviceCsr, Probe, Workspace, cached_device_csr, current_stream
+from .device import (DeviceCsr, Probe, Workspace, cached_device_csr, current_stream, device_to_host,
+                     host_to_device)
 from .executor import ExecutorConfig
 from .schedules import ScheduleKind
 
@@ -115,10 +116,10 @@ def spmv(m, x, cfg: ExecutorConfig | None = None, *, out=None, dtype=None):
     if xh.ndim != 1 or xh.size != m.cols:
         raise ValueError(f"x has length {xh.size}, expected {m.cols}")
     dm = cached_device_csr(m, dtype=dtype or "float64")
-    xd = torch.from_numpy(xh).to(dm.device).to(dm.dtype)
+    xd = host_to_device(xh, dm.device, dm.dtype)
     y = torch.empty(dm.rows, dtype=dm.dtype, device=dm.device)
     _launch(dm, xd, y, cfg, None, current_stream(dm.device))
-    return y.to(torch.float64).cpu().numpy()
+    return device_to_host(y.to(torch.float64))
 
 
 def _launch_spmm(m: DeviceCsr, B, C, cfg: ExecutorConfig, stream: int) -> None:
@@ -168,10 +169,10 @@ def spmm(m, B, cfg: ExecutorConfig | None = None, *, out=None, dtype=None):
     if Bh.ndim != 2 or Bh.shape[0] != m.cols:
         raise ValueError(f"B has shape {Bh.shape}, expected ({m.cols}, k)")
     dm = cached_device_csr(m, dtype=dtype or "float64")
-    Bd = torch.from_numpy(Bh).to(dm.device).to(dm.dtype)
+    Bd = host_to_device(Bh, dm.device, dm.dtype)
     C = torch.empty((dm.rows, Bh.shape[1]), dtype=dm.dtype, device=dm.device)
     _launch_spmm(dm, Bd, C, cfg, current_stream(dm.device))
-    return C.to(torch.float64).cpu().numpy()
+    return device_to_host(C.to(torch.float64))
 
 
 def spmv_probe(m: DeviceCsr, x, cfg: ExecutorConfig | None = None):
