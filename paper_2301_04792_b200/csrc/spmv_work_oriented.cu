@@ -20,7 +20,6 @@
 //     (executor.py:212-221). Runs of carries into one row are summed in order,
 //     so results are run-to-run reproducible (no float atomics).
 #include <algorithm>
-#include <type_traits>
 #include <climits>
 #include <cstdlib>
 
@@ -465,191 +464,6 @@ __global__ void __launch_bounds__(WoCfg<ValT>::NT)
     }
 }
 
-// ---- 2b. shared-memory x tier (persistent, fp32, hot-x packed operands) -----------
-// The chunk kernel above is bound by the SM's L1->L2 request rate: every x
-// gather that misses L1 costs one request. Here the packed hot
-// values xh[0, n_tier) — the most gathered columns, relabelled by lw_hotx_build —
-// are copied ONCE per CTA into shared memory, so those gathers (36% of C3's at
-// 32 K slots) cost no request at all; hot slots beyond the tier stay in L1
-// (evict_last) and cold gathers allocate in L1 normally. Amortising the copy
-// needs long-lived CTAs: one CTA per SM holding G independent groups of NT
-// threads; group g of CTA b walks the partition's lanes b*G + g, b*G + g +
-// grid*G, ... (neighbouring CTAs on neighbouring lanes, like the one-shot
-// launch). A group runs exactly the chunk body of k_wo_chunk on its lane with
-// named barriers (bar.sync 1+g, NT) instead of __syncthreads, so the groups'
-// gather and scan phases interleave on the SM. Same partition, same per-chunk
-// arithmetic, same carries: y is bit-identical to k_wo_chunk's.
-template <int NT>
-__device__ __forceinline__ void group_bar(int id) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(NT) : "memory");
-}
-
-template <class OffT, int NT, int G, bool VEC>
-__global__ void __launch_bounds__(NT * G, 1)
-    k_wo_tier(Csr<OffT, float> A, const float* __restrict__ x, float* __restrict__ y, int64_t items,
-              int64_t J, int64_t lanes, const int64_t* __restrict__ bound_tile,
-              int64_t* __restrict__ carry_tile, double* __restrict__ carry_val,
-              const float* __restrict__ xh, int32_t n_hot, int32_t n_tier) {
-    constexpr int IPT = WO_W / NT;
-    constexpr int W = WO_W, S = WO_S;
-    static_assert(NT * IPT == W && IPT % 4 == 0, "window must be NT*IPT atoms");
-    using SM = WoSmem<float>;
-    extern __shared__ __align__(16) unsigned char sm[];
-    __shared__ WoScan<NT> scans[G];
-    float* s_tier = reinterpret_cast<float*>(sm);
-    const int g = threadIdx.x / NT, tid = threadIdx.x - g * NT;
-    unsigned char* gsm = sm + ((size_t)n_tier * 4 + 15) / 16 * 16 + (size_t)g * ((SM::bytes + 15) / 16 * 16);
-    uint16_t* s_end = reinterpret_cast<uint16_t*>(gsm + SM::end_off);
-    float* s_seg = reinterpret_cast<float*>(gsm + SM::seg_off);
-    uint32_t* s_flag = reinterpret_cast<uint32_t*>(gsm + SM::flag_off);
-    WoScan<NT>& scan = scans[g];
-    const int bar = 1 + g;
-
-    for (int i = threadIdx.x; i < n_tier; i += NT * G) s_tier[i] = xh[i];
-    __syncthreads();
-
-    const int lane = tid & (kWarp - 1), warp = tid >> 5;
-    const int64_t total = A.rows + A.nnz;
-    for (int64_t l = (int64_t)blockIdx.x * G + g; l < lanes; l += (int64_t)gridDim.x * G) {
-        const int64_t lane_d0 = l * items;
-        int64_t run_row = -1;
-        double run_val = 0.0;
-        bool run_has = false;
-        for (int64_t jc = 0; jc < J; ++jc) {
-            const int64_t d0 = min(lane_d0 + min(jc * S, items), total);
-            const int64_t d1 = min(lane_d0 + min((jc + 1) * S, items), total);
-            if (d0 >= d1) break;
-            const int64_t t0 = bound_tile[l * J + jc], t1 = bound_tile[l * J + jc + 1];
-            const int64_t a0 = d0 - t0;
-            const int n_rows = (int)(t1 - t0), n_atoms = (int)((d1 - t1) - a0);
-            const int64_t base = a0 & ~(int64_t)7;
-            const int w0 = (int)(a0 - base);
-            const int w1 = w0 + n_atoms;
-            if (tid <= W / 32 + 1) s_flag[tid] = 0u;
-
-            const int pos = IPT * tid;
-            const int64_t gi = base + pos;
-            float p[IPT];
-            const bool row0 = tid < n_rows;
-            int32_t e0 = 0;
-            {
-                int32_t c[IPT];
-                float v[IPT];
-#pragma unroll
-                for (int k = 0; k < IPT; ++k) { c[k] = (int32_t)0x80000000; v[k] = 0.f; }
-                if (pos < w1) {
-                    if (VEC && gi + IPT <= A.nnz) {
-                        ld_atoms<IPT>(A.col + gi, A.val + gi, c, v);
-                    } else {
-#pragma unroll
-                        for (int k = 0; k < IPT; ++k)
-                            if (gi + k < A.nnz) { c[k] = ld_stream(A.col + gi + k); v[k] = ld_stream(A.val + gi + k); }
-                    }
-                }
-                if (row0) e0 = (int32_t)(ld_off(A.off + t0 + 1 + tid) - base);
-#pragma unroll
-                for (int k = 0; k < IPT; ++k) {
-                    const int32_t ck = c[k];
-                    if (ck < 0) {
-                        const int sl = ck & 0x7fffffff;
-                        if (sl < n_tier) p[k] = s_tier[sl];
-                        else LW_LDASM("ld.global.nc.L1::evict_last.f32 %0, [%1];" : "=f"(p[k]) : "l"(xh + sl));
-                    } else {
-                        LW_LDASM("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;"
-                                 : "=f"(p[k]) : "l"(x + ck), "l"(policy_evict_last()));
-                    }
-                }
-#pragma unroll
-                for (int k = 0; k < IPT; ++k) {
-                    const bool in = pos + k >= w0 && pos + k < w1;
-                    p[k] = in ? v[k] * p[k] : 0.f;
-                }
-            }
-
-            group_bar<NT>(bar);
-            if (row0) {
-                s_end[tid] = e0;
-                if (e0 < W) atomicOr(&s_flag[e0 >> 5], 1u << (e0 & 31));
-            }
-            for (int i = tid + NT; i < n_rows; i += NT) {
-                const int e = (int)(ld_off(A.off + t0 + 1 + i) - base);
-                s_end[i] = e;
-                if (e < W) atomicOr(&s_flag[e >> 5], 1u << (e & 31));
-            }
-            group_bar<NT>(bar);
-
-            uint32_t fl;
-            {
-                const uint64_t two = ((uint64_t)s_flag[(pos >> 5) + 1] << 32) | s_flag[pos >> 5];
-                fl = (uint32_t)(two >> (pos & 31)) & (uint32_t)((1ull << IPT) - 1ull);
-            }
-            bool has = fl != 0u;
-            float run = 0.f;
-#pragma unroll
-            for (int k = 0; k < IPT; ++k) run = ((fl >> k) & 1u) ? p[k] : run + p[k];
-#pragma unroll
-            for (int d = 1; d < kWarp; d <<= 1) {
-                const float ov = shfl_up(run, d);
-                const int oh = shfl_up((int)has, d);
-                if (lane >= d) {
-                    if (!has) run += ov;
-                    has = has || oh;
-                }
-            }
-            if (lane == kWarp - 1) { scan.has[warp] = has; scan.val[warp] = (double)run; }
-            group_bar<NT>(bar);
-            float wpre = 0.f;
-            {
-                bool h = false;
-                for (int w = warp - 1; w >= 0 && !h; --w) {
-                    wpre += (float)scan.val[w];
-                    h = scan.has[w];
-                }
-            }
-            float cin = shfl_up(run, 1);
-            const int hin = shfl_up((int)has, 1);
-            if (lane == 0) cin = wpre;
-            else if (!hin) cin += wpre;
-            {
-                float r = cin;
-#pragma unroll
-                for (int k = 0; k < IPT; ++k) {
-                    r = ((fl >> k) & 1u) ? p[k] : r + p[k];
-                    p[k] = r;
-                }
-                store_run<IPT>(s_seg + pos, p);
-            }
-            group_bar<NT>(bar);
-
-            for (int i = tid; i < n_rows; i += NT) {
-                const int e = s_end[i];
-                const int st = i ? s_end[i - 1] : w0;
-                double v = e > st ? (double)s_seg[e - 1] : 0.0;
-                if (i == 0 && run_has && run_row == t0) v += run_val;
-                y[t0 + i] = (float)v;
-            }
-            {
-                const int st = n_rows ? s_end[n_rows - 1] : w0;
-                const bool tail = w1 > st;
-                const double tv = tail ? (double)s_seg[w1 - 1] : 0.0;
-                if (n_rows > 0) {
-                    run_row = t1; run_val = tv; run_has = tail;
-                } else if (run_has && run_row == t1) {
-                    run_val += tv;
-                } else {
-                    run_row = t1; run_val = tv; run_has = tail;
-                }
-            }
-            group_bar<NT>(bar);   // s_end / s_seg / s_flag / scan are rewritten by the next chunk
-        }
-        if (tid == 0) {
-            const bool live = run_has && run_row >= 0 && run_row < A.rows;
-            carry_tile[l] = live ? run_row : -1;
-            carry_val[l] = live ? run_val : 0.0;
-        }
-    }
-}
-
 // ---- 3. ordered carry fix-up -----------------------------------------------------
 template <class ValT, bool PEERS = false>
 __global__ void k_carry_fixup(const int64_t* __restrict__ carry_tile,
@@ -778,10 +592,6 @@ int merge_path_partition(int64_t rows, int64_t nnz, const void* off, int bits, i
                                   coords, s);
 }
 
-static int env_int(const char* name, int dflt) {
-    const char* v = getenv(name);
-    return v ? atoi(v) : dflt;
-}
 
 template <class OffT, class ValT, bool PR, bool VEC, bool HOT = false>
 static int launch_chunk(const Csr<OffT, ValT>& a, const ValT* x, ValT* y, const WoPlan& p,
@@ -800,50 +610,6 @@ static int launch_chunk(const Csr<OffT, ValT>& a, const ValT* x, ValT* y, const 
                                                          c_val, pr, PeerOut{}, xh);
     LW_LAUNCH_CHECK();
     return LW_OK;
-}
-
-// Shared-memory tier launch (k_wo_tier): one CTA per SM, G groups of NT threads.
-// LW_WO_TIER=0 falls back to the one-shot chunk kernel; LW_WO_TIER_MAX caps the
-// tier (slots); LW_WO_TIER_SHAPE picks the group shape (A/B runs only).
-
-template <class OffT, int NT, int G, bool VEC>
-static int launch_tier_shape(const Csr<OffT, float>& a, const float* x, float* y, const WoPlan& p,
-                             const int64_t* tiles, int64_t* c_tile, double* c_val, const float* xh,
-                             int32_t n_hot, cudaStream_t s) {
-    auto kern = k_wo_tier<OffT, NT, G, VEC>;
-    constexpr size_t stage = (WoSmem<float>::bytes + 15) / 16 * 16;
-    static int max_dyn = -1;
-    if (max_dyn < 0) {
-        int dev = 0, optin = 0;
-        LW_TRY(cudaGetDevice(&dev));
-        LW_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-        cudaFuncAttributes fa{};
-        LW_TRY(cudaFuncGetAttributes(&fa, kern));
-        max_dyn = optin - (int)fa.sharedSizeBytes;
-        LW_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn));
-    }
-    const int64_t cap = ((int64_t)max_dyn - (int64_t)G * (int64_t)stage - 16) / 4;
-    int32_t n_tier = (int32_t)std::min<int64_t>(std::min<int64_t>(n_hot, cap),
-                                                env_int("LW_WO_TIER_MAX", 1 << 30));
-    if (n_tier < 0) n_tier = 0;
-    const size_t smem = ((size_t)n_tier * 4 + 15) / 16 * 16 + (size_t)G * stage;
-    const int64_t grid = std::min<int64_t>(ceil_div(p.lanes, (int64_t)G), (int64_t)sm_count());
-    kern<<<(unsigned)std::max<int64_t>(grid, 1), NT * G, smem, s>>>(a, x, y, p.items, p.J, p.lanes, tiles,
-                                                                  c_tile, c_val, xh, n_hot, n_tier);
-    LW_LAUNCH_CHECK();
-    return LW_OK;
-}
-
-template <class OffT, bool VEC>
-static int launch_tier(const Csr<OffT, float>& a, const float* x, float* y, const WoPlan& p,
-                       const int64_t* tiles, int64_t* c_tile, double* c_val, const float* xh,
-                       int32_t n_hot, cudaStream_t s) {
-    switch (env_int("LW_WO_TIER_SHAPE", 0)) {
-        case 1: return launch_tier_shape<OffT, 256, 4, VEC>(a, x, y, p, tiles, c_tile, c_val, xh, n_hot, s);
-        case 2: return launch_tier_shape<OffT, 512, 1, VEC>(a, x, y, p, tiles, c_tile, c_val, xh, n_hot, s);
-        case 3: return launch_tier_shape<OffT, 256, 2, VEC>(a, x, y, p, tiles, c_tile, c_val, xh, n_hot, s);
-        default: return launch_tier_shape<OffT, 512, 2, VEC>(a, x, y, p, tiles, c_tile, c_val, xh, n_hot, s);
-    }
 }
 
 template <class OffT, class ValT>
@@ -886,14 +652,6 @@ static int launch_wo(const lw_csr_t* A, const void* x, void* y, const WoPlan& p,
         if (hot_cols) {   // packed hot x lives after the carries in the workspace
             ValT* xh = (ValT*)(w + align_up(nb * 8, 256) + 2 * align_up(nc * 8, 256));
             // (xh was packed by the partition phase's launch, k_search_pack)
-            if constexpr (std::is_same<ValT, float>::value) {
-                if (env_int("LW_WO_TIER", 1) != 0 && n_hot > 0) {
-                    rc = vec ? launch_tier<OffT, true>(a, xv, yv, p, tiles, c_tile, c_val, xh, n_hot, s)
-                             : launch_tier<OffT, false>(a, xv, yv, p, tiles, c_tile, c_val, xh, n_hot, s);
-                    if (rc) return rc;
-                    goto spmv_done;
-                }
-            }
             rc = vec ? launch_chunk<OffT, ValT, false, true, true>(a, xv, yv, p, tiles, c_tile, c_val, pr, s, xh)
                      : launch_chunk<OffT, ValT, false, false, true>(a, xv, yv, p, tiles, c_tile, c_val, pr, s, xh);
         } else if (P) rc = vec ? launch_chunk<OffT, ValT, true, true>(a, xv, yv, p, tiles, c_tile, c_val, pr, s)
@@ -903,7 +661,6 @@ static int launch_wo(const lw_csr_t* A, const void* x, void* y, const WoPlan& p,
         if (rc) return rc;
         LW_LAUNCH_CHECK();
     }
-spmv_done:
     if (phases & WO_PHASE_FIXUP) {
         k_carry_fixup<ValT><<<ceil_div(n_carry, 256), 256, 0, s>>>(c_tile, c_val, n_carry, (ValT*)y, a.rows);
         LW_LAUNCH_CHECK();
