@@ -70,8 +70,10 @@ template <class OffT>
 __global__ void k_merge_path_search(const OffT* __restrict__ off, int64_t rows, int64_t nnz,
                                     int64_t n_bounds, int64_t J, int64_t items, int64_t S,
                                     int64_t* __restrict__ out_tile,
-                                    int64_t* __restrict__ out_coords) {
+                                    int64_t* __restrict__ out_coords,
+                                    unsigned* __restrict__ ticket = nullptr) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (ticket && k == 0) *ticket = 0u;   // the carry fix-up's CTA counter
     if (k >= n_bounds) return;
     const int64_t d = wo_bound_diag(k, J, items, S, rows + nnz);
     int64_t lo = max((int64_t)0, d - nnz), hi = min(d, rows);
@@ -465,32 +467,131 @@ __global__ void __launch_bounds__(WoCfg<ValT>::NT)
 }
 
 // ---- 3. ordered carry fix-up -----------------------------------------------------
+// Adds every lane's carry-out to its row (reference kernels.py:90-91: serial,
+// in lane order). Carry rows are nondecreasing along the path with sentinels
+// (-1) where a lane ended on a row boundary, so each row's carries form one
+// contiguous run. Runs are summed by a segmented reduction, never by a walk:
+// each CTA scans FX_NT consecutive carries (warp shuffles, then across warps);
+// a run that starts and ends inside the CTA is added to y by its last carry's
+// thread; the (at most two) run pieces that touch the CTA's edges are recorded
+// and the last CTA to finish (atomic ticket) adds the runs that cross CTAs in
+// path order. Every row is updated by exactly one thread, no float atomics:
+// y is run-to-run reproducible, and a row spanning all 68 K lanes costs the
+// same as any other (one scan step), where a per-row walk would be serial.
+constexpr int FX_NT = 1024;
+struct FixSeg {
+    int64_t key;   // row, or -2 = empty slot
+    double sum;
+};
+
+__device__ __forceinline__ int64_t fx_key(const int64_t* __restrict__ t, int64_t i, int64_t rows) {
+    const int64_t r = t[i];
+    return (r >= 0 && r < rows) ? r : -1;
+}
+
 template <class ValT, bool PEERS = false>
-__global__ void k_carry_fixup(const int64_t* __restrict__ carry_tile,
-                              const double* __restrict__ carry_val, int64_t n,
-                              ValT* __restrict__ y, int64_t rows, PeerOut po = PeerOut{}) {
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    const int64_t r = carry_tile[k];
-    if (r < 0 || r >= rows) return;
-    // Carry rows are nondecreasing along the path, with sentinels (-1) wherever
-    // a lane/warp ended on a row boundary; the head of a row's run is its first
-    // non-sentinel carry and it alone updates y[r] (no float atomics).
-    for (int64_t m = k - 1; m >= 0; --m) {
-        const int64_t t = carry_tile[m];
-        if (t == r) return;   // not the head of its run
-        if (t >= 0) break;
+__global__ void __launch_bounds__(FX_NT)
+    k_carry_fixup(const int64_t* __restrict__ carry_tile, const double* __restrict__ carry_val,
+                  int64_t n, ValT* __restrict__ y, int64_t rows, unsigned* __restrict__ ticket,
+                  FixSeg* __restrict__ segs, PeerOut po = PeerOut{}) {
+    __shared__ double s_sum[FX_NT / kWarp];
+    __shared__ int s_has[FX_NT / kWarp];
+    __shared__ bool s_last;
+    const int tid = threadIdx.x, lane = tid & (kWarp - 1), warp = tid >> 5;
+    const int64_t c0 = (int64_t)blockIdx.x * FX_NT, c1 = min(c0 + FX_NT, n), i = c0 + tid;
+    const bool in = i < c1;
+    const int64_t key = in ? fx_key(carry_tile, i, rows) : -3;
+    const double v = in && key >= 0 ? carry_val[i] : 0.0;
+    // neighbours' keys from the warp, the warp-edge ones from memory
+    int64_t prev = shfl_up(key, 1), next = __shfl_down_sync(0xffffffffu, key, 1);
+    if (lane == 0) prev = i > 0 && in ? fx_key(carry_tile, i - 1, rows) : -4;
+    if (lane == kWarp - 1 || i + 1 >= c1) next = i + 1 < n ? fx_key(carry_tile, i + 1, rows) : -5;
+    // head: first carry of its run; the CTA's first carry is a head only if the
+    // run really starts there
+    const bool head = in && (i == 0 || prev != key);
+    const bool brk = in && (i == c0 || head);   // scan segment boundary
+    const bool tail = in && next != key;
+    if (tid < 2) segs[2 * blockIdx.x + tid] = FixSeg{-2, 0.0};
+
+    // segmented inclusive scan of v (segments start at brk) + "a head in my segment"
+    double run = v;
+    bool has = brk, hh = head;   // hh: the segment's start is a true run head
+    for (int d = 1; d < kWarp; d <<= 1) {
+        const double ov = shfl_up(run, d);
+        const int oh = shfl_up((int)has, d);
+        const int ohh = shfl_up((int)hh, d);
+        if (lane >= d && !has) {
+            run += ov;
+            has = oh;
+            hh = ohh;
+        }
     }
-    double s = 0.0;
-    for (int64_t m = k; m < n; ++m) {
-        const int64_t t = carry_tile[m];
-        if (t < 0) continue;
-        if (t != r) break;
-        s += carry_val[m];
+    if (lane == kWarp - 1) { s_sum[warp] = run; s_has[warp] = has ? (hh ? 2 : 1) : 0; }
+    __syncthreads();
+    if (!has) {   // my segment started in an earlier warp
+        for (int w = warp - 1; w >= 0; --w) {
+            run += s_sum[w];
+            if (s_has[w]) { hh = s_has[w] == 2; break; }
+        }
     }
-    const ValT v = (ValT)((double)y[r] + s);
-    y[r] = v;
-    if (PEERS) peer_store(po, po.ptr, r, v);
+    const bool last_in_cta = in && i == c1 - 1;
+    if (in && key >= 0) {
+        if (tail && hh) {                       // the whole run is inside this CTA
+            const ValT out = (ValT)((double)y[key] + run);
+            y[key] = out;
+            if (PEERS) peer_store(po, po.ptr, key, out);
+        } else if (tail && !hh) {               // piece that started before this CTA
+            segs[2 * blockIdx.x] = FixSeg{key, run};
+        } else if (last_in_cta) {               // piece that continues into the next CTA
+            segs[2 * blockIdx.x + (hh ? 1 : 0)] = FixSeg{key, run};
+        }
+    }
+    // the last CTA to finish adds the runs that cross CTAs, in path order
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // stage the pieces through shared memory (coalesced, all threads), then one
+    // thread merges them in path order
+    __shared__ int64_t s_key[FX_NT];
+    __shared__ double s_val[FX_NT];
+    int64_t cur = -2;
+    double acc = 0.0;
+    const int64_t ns = 2 * (int64_t)gridDim.x;
+    for (int64_t base = 0; base < ns; base += FX_NT) {
+        const int64_t k = base + tid;
+        s_key[tid] = k < ns ? __ldcg(&segs[k].key) : -2;
+        s_val[tid] = k < ns ? __ldcg(&segs[k].sum) : 0.0;
+        __syncthreads();
+        if (tid == 0) {
+            const int m = (int)min((int64_t)FX_NT, ns - base);
+            for (int j = 0; j < m; ++j) {
+                const int64_t kk = s_key[j];
+                if (kk == -2) continue;
+                if (kk != cur) {
+                    if (cur >= 0) {
+                        const ValT out = (ValT)((double)y[cur] + acc);
+                        y[cur] = out;
+                        if (PEERS) peer_store(po, po.ptr, cur, out);
+                    }
+                    cur = kk;
+                    acc = 0.0;
+                }
+                acc += s_val[j];
+            }
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        if (cur >= 0) {
+            const ValT out = (ValT)((double)y[cur] + acc);
+            y[cur] = out;
+            if (PEERS) peer_store(po, po.ptr, cur, out);
+        }
+        *ticket = 0u;   // ready for the next launch on this workspace
+    }
 }
 
 // ---- 4. hot-x pack: xh[slot] = x[hot_cols[slot]] (n_hot gathers per call) ----------------
@@ -508,7 +609,8 @@ __global__ void k_search_pack(const OffT* __restrict__ off, int64_t rows, int64_
                               int64_t n_bounds, int64_t J, int64_t items, int64_t S,
                               int64_t* __restrict__ out_tile, unsigned nsb,
                               const ValT* __restrict__ x, const int32_t* __restrict__ hot_cols,
-                              int32_t n_hot, ValT* __restrict__ xh) {
+                              int32_t n_hot, ValT* __restrict__ xh, unsigned* __restrict__ ticket) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *ticket = 0u;
     if (blockIdx.x >= nsb) {
         const int i = (int)(blockIdx.x - nsb) * blockDim.x + threadIdx.x;
         if (i < n_hot) xh[i] = x[hot_cols[i]];
@@ -546,10 +648,53 @@ static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 // carry slots: one per lane
 static size_t wo_carries(const WoPlan& p) { return (size_t)p.lanes; }
 
+// Workspace: chunk-boundary tiles, carry rows, carry values, the fix-up's
+// ticket + edge pieces (2 per fix-up CTA); the hot-x variant appends xh.
+struct WoWs {
+    int64_t* tiles;
+    int64_t* c_tile;
+    double* c_val;
+    unsigned* ticket;
+    FixSeg* segs;
+    unsigned char* end;
+};
+
+static size_t wo_fix_bytes(const WoPlan& p) {
+    const size_t blocks = (size_t)ceil_div((int64_t)wo_carries(p), (int64_t)FX_NT);
+    return align_up(16 + 2 * (blocks > 0 ? blocks : 1) * sizeof(FixSeg), 256);
+}
+
+static WoWs wo_ws(const WoPlan& p, void* ws) {
+    const size_t nb = (size_t)(p.lanes * p.J + 1), nc = wo_carries(p);
+    unsigned char* w = (unsigned char*)ws;
+    WoWs r{};
+    r.tiles = (int64_t*)w;
+    w += align_up(nb * 8, 256);
+    r.c_tile = (int64_t*)w;
+    w += align_up(nc * 8, 256);
+    r.c_val = (double*)w;
+    w += align_up(nc * 8, 256);
+    r.ticket = (unsigned*)w;
+    r.segs = (FixSeg*)(w + 16);
+    w += wo_fix_bytes(p);
+    r.end = w;
+    return r;
+}
+
 size_t wo_workspace(int64_t rows, int64_t nnz, int64_t lanes) {
     const WoPlan p = wo_plan(rows, nnz, lanes);
     const size_t nb = (size_t)(p.lanes * p.J + 1), nc = wo_carries(p);
-    return align_up(nb * 8, 256) + align_up(nc * 8, 256) + align_up(nc * 8, 256);
+    return align_up(nb * 8, 256) + 2 * align_up(nc * 8, 256) + wo_fix_bytes(p);
+}
+
+template <class ValT, bool PEERS = false>
+static int launch_fixup(const WoWs& w, int64_t n, ValT* y, int64_t rows, cudaStream_t s,
+                        const PeerOut& po = PeerOut{}) {
+    if (n <= 0) return LW_OK;
+    k_carry_fixup<ValT, PEERS><<<(unsigned)ceil_div(n, (int64_t)FX_NT), FX_NT, 0, s>>>(
+        w.c_tile, w.c_val, n, y, rows, w.ticket, w.segs, po);
+    LW_LAUNCH_CHECK();
+    return LW_OK;
 }
 
 int64_t wo_lanes(int64_t rows, int64_t nnz, int64_t lanes) { return wo_plan(rows, nnz, lanes).lanes; }
@@ -557,10 +702,10 @@ int64_t wo_lanes(int64_t rows, int64_t nnz, int64_t lanes) { return wo_plan(rows
 template <class OffT>
 static int launch_search(const OffT* off, int64_t rows, int64_t nnz, int64_t n_bounds, int64_t J,
                          int64_t items, int64_t S, int64_t* out_tile, int64_t* out_coords,
-                         cudaStream_t s) {
+                         cudaStream_t s, unsigned* ticket = nullptr) {
     const int NT = 256;
     k_merge_path_search<OffT><<<ceil_div(n_bounds, NT), NT, 0, s>>>(off, rows, nnz, n_bounds, J, items,
-                                                                 S, out_tile, out_coords);
+                                                                 S, out_tile, out_coords, ticket);
     LW_LAUNCH_CHECK();
     return LW_OK;
 }
@@ -618,29 +763,29 @@ static int launch_wo(const lw_csr_t* A, const void* x, void* y, const WoPlan& p,
                      const int32_t* hot_cols = nullptr, int32_t n_hot = 0) {
     Csr<OffT, ValT> a{A->rows, A->cols, A->nnz, (const OffT*)A->row_offsets,
                       A->col_indices, (const ValT*)A->values};
-    const size_t nb = (size_t)(p.lanes * p.J + 1), nc = wo_carries(p);
-    unsigned char* w = (unsigned char*)ws;
-    int64_t* tiles = (int64_t*)w;
-    int64_t* c_tile = (int64_t*)(w + align_up(nb * 8, 256));
-    double* c_val = (double*)(w + align_up(nb * 8, 256) + align_up(nc * 8, 256));
+    const size_t nb = (size_t)(p.lanes * p.J + 1);
+    const WoWs W = wo_ws(p, ws);
+    int64_t* tiles = W.tiles;
+    int64_t* c_tile = W.c_tile;
+    double* c_val = W.c_val;
+    ValT* xh = (ValT*)W.end;   // hot-x variant only: packed hot values after the base workspace
     Probe pr{};
     if (probe) pr = Probe{probe->lane_atoms, probe->atom_lane, probe->atom_tile, probe->atom_visits};
     if (p.lanes > 0x7fffffff) return LW_E_UNSUPPORTED;
     // 32-byte vector loads need 32-byte aligned col_idx / values
     const bool vec = ((uintptr_t)A->col_indices % 32 == 0) && ((uintptr_t)A->values % 32 == 0);
-    const int64_t n_carry = p.lanes;   // the fix-up walks one carry per lane
+    const int64_t n_carry = p.lanes;   // one carry per lane
 
     if ((phases & WO_PHASE_PARTITION) && hot_cols && n_hot > 0) {   // partition + hot-x pack
-        ValT* xh = (ValT*)(w + align_up(nb * 8, 256) + 2 * align_up(nc * 8, 256));
         const unsigned nsb = (unsigned)ceil_div((int64_t)nb, 256);
         const unsigned npb = (unsigned)ceil_div(n_hot, 256);
         k_search_pack<OffT, ValT><<<nsb + npb, 256, 0, s>>>(a.off, a.rows, a.nnz, (int64_t)nb, p.J, p.items,
                                                           WO_S, tiles, nsb, (const ValT*)x, hot_cols,
-                                                          n_hot, xh);
+                                                          n_hot, xh, W.ticket);
         LW_LAUNCH_CHECK();
     } else if (phases & WO_PHASE_PARTITION) {
         int rc = launch_search<OffT>(a.off, a.rows, a.nnz, (int64_t)nb, p.J, p.items, WO_S, tiles,
-                                     nullptr, s);
+                                     nullptr, s, W.ticket);
         if (rc) return rc;
     }
     if (phases & WO_PHASE_SPMV) {
@@ -649,8 +794,7 @@ static int launch_wo(const lw_csr_t* A, const void* x, void* y, const WoPlan& p,
         ValT* yv = (ValT*)y;
         const bool P = probe != nullptr;
         int rc = LW_OK;
-        if (hot_cols) {   // packed hot x lives after the carries in the workspace
-            ValT* xh = (ValT*)(w + align_up(nb * 8, 256) + 2 * align_up(nc * 8, 256));
+        if (hot_cols) {   // packed hot x lives after the base workspace
             // (xh was packed by the partition phase's launch, k_search_pack)
             rc = vec ? launch_chunk<OffT, ValT, false, true, true>(a, xv, yv, p, tiles, c_tile, c_val, pr, s, xh)
                      : launch_chunk<OffT, ValT, false, false, true>(a, xv, yv, p, tiles, c_tile, c_val, pr, s, xh);
@@ -662,8 +806,8 @@ static int launch_wo(const lw_csr_t* A, const void* x, void* y, const WoPlan& p,
         LW_LAUNCH_CHECK();
     }
     if (phases & WO_PHASE_FIXUP) {
-        k_carry_fixup<ValT><<<ceil_div(n_carry, 256), 256, 0, s>>>(c_tile, c_val, n_carry, (ValT*)y, a.rows);
-        LW_LAUNCH_CHECK();
+        int rc = launch_fixup<ValT>(W, n_carry, (ValT*)y, a.rows, s);
+        if (rc) return rc;
     }
     return LW_OK;
 }
@@ -675,20 +819,21 @@ static int launch_wo_peers(const lw_csr_t* A, const void* x, void* y, const WoPl
     Csr<OffT, ValT> a{A->rows, A->cols, A->nnz, (const OffT*)A->row_offsets, A->col_indices,
                       (const ValT*)A->values};
     const size_t nb = (size_t)(p.lanes * p.J + 1);
-    unsigned char* w = (unsigned char*)ws;
-    int64_t* tiles = (int64_t*)w;
-    int64_t* c_tile = (int64_t*)(w + align_up(nb * 8, 256));
-    double* c_val = (double*)(w + align_up(nb * 8, 256) + align_up(wo_carries(p) * 8, 256));
+    const WoWs W = wo_ws(p, ws);
+    int64_t* tiles = W.tiles;
+    int64_t* c_tile = W.c_tile;
+    double* c_val = W.c_val;
     if (p.lanes > 0x7fffffff) return LW_E_UNSUPPORTED;
-    int rc = launch_search<OffT>(a.off, a.rows, a.nnz, (int64_t)nb, p.J, p.items, WO_S, tiles, nullptr, s);
+    int rc = launch_search<OffT>(a.off, a.rows, a.nnz, (int64_t)nb, p.J, p.items, WO_S, tiles, nullptr, s,
+                                 W.ticket);
     if (rc) return rc;
     const bool vec = ((uintptr_t)A->col_indices % 32 == 0) && ((uintptr_t)A->values % 32 == 0);
     constexpr size_t smem = WoSmem<ValT>::bytes;
     auto kern = vec ? k_wo_chunk<OffT, ValT, false, true, true, HOT>
                     : k_wo_chunk<OffT, ValT, false, false, true, HOT>;
     ValT* xh = nullptr;
-    if constexpr (HOT) {   // packed hot x after the carries, as in launch_wo
-        xh = (ValT*)(w + align_up(nb * 8, 256) + 2 * align_up(wo_carries(p) * 8, 256));
+    if constexpr (HOT) {   // packed hot x after the base workspace, as in launch_wo
+        xh = (ValT*)W.end;
         if (n_hot > 0) {
             k_hot_pack<ValT><<<(unsigned)ceil_div(n_hot, 256), 256, 0, s>>>((const ValT*)x, hot_cols, n_hot, xh);
             LW_LAUNCH_CHECK();
@@ -702,10 +847,7 @@ static int launch_wo_peers(const lw_csr_t* A, const void* x, void* y, const WoPl
     kern<<<(unsigned)p.lanes, WoCfg<ValT>::NT, smem, s>>>(a, (const ValT*)x, (ValT*)y, p.items, p.J,
                                                          tiles, c_tile, c_val, Probe{}, po, xh);
     LW_LAUNCH_CHECK();
-    k_carry_fixup<ValT, true><<<ceil_div(p.lanes, 256), 256, 0, s>>>(c_tile, c_val, p.lanes, (ValT*)y,
-                                                                     a.rows, po);
-    LW_LAUNCH_CHECK();
-    return LW_OK;
+    return launch_fixup<ValT, true>(W, p.lanes, (ValT*)y, a.rows, s, po);
 }
 
 size_t wo_hotx_workspace(int64_t rows, int64_t nnz, int64_t lanes, int64_t n_hot, int dtype);
