@@ -147,6 +147,16 @@ int lw_spmv_work_oriented_phases(const lw_csr_t* A, const void* x, void* y, int6
  * = |H|. lw_spmv_work_oriented_hotx: A's col_indices must be col_packed; packs
  * xh[s] = x[hot_cols[s]] into the workspace, then runs the work_oriented SpMV
  * with hot gathers kept in L1 and cold ones bypassing it. */
+/* Symmetric permutation P A P^T of a square CSR (degree relabeling for the
+ * iterated SpMV, C5): output row i is input row order[i] with every column c
+ * renamed rank[c] (rank = order^-1, device int32[cols]; order device
+ * int64[rows]); atoms keep their order inside a row. off_out (rows+1 entries,
+ * the input's offset width) is the caller's prefix sum of the permuted row
+ * lengths; col_out / val_out hold nnz entries. One-time inspector step; no
+ * reference counterpart (the reference iterates in the input numbering). */
+int lw_csr_permute(const lw_csr_t* A, const int64_t* order, const int32_t* rank, const void* off_out,
+                   int32_t* col_out, void* val_out, uintptr_t stream);
+
 size_t lw_hotx_build_workspace(int64_t cols);
 int lw_hotx_build(const lw_csr_t* A, int32_t max_hot, int32_t* col_packed, int32_t* hot_cols,
                   int32_t* n_hot_out, void* workspace, size_t workspace_bytes, uintptr_t stream);
@@ -188,7 +198,8 @@ int lw_spmv_work_oriented_peers_hotx(const lw_csr_t* A_packed, const int32_t* ho
 /* Power-iteration normalisation (BASELINE C5; the reference driver's x = y/||y||):
  * lw_vector_norm writes ||y||_2 (fp64, deterministic two-level reduction) to the
  * DEVICE scalar norm_out; lw_vector_scale writes x = y / norm (x = y when the
- * norm is 0) reading the device scalar, so the pair runs without a host sync.
+ * norm is 0) reading the device scalar, so the pair runs without a host sync;
+ * x may equal y (in-place).
  * Workspace: lw_norm_workspace(n) bytes of device memory. */
 size_t lw_norm_workspace(int64_t n);
 int lw_vector_norm(const void* y, int64_t n, int32_t dtype, void* workspace,

@@ -72,6 +72,7 @@ EXPORTS = (
     "lw_rmat_keys",
     "lw_hash_values",
     "lw_uniform_keys",
+    "lw_csr_permute",
 )
 
 
@@ -182,6 +183,7 @@ _SIGNATURES = {
     "lw_rmat_keys": (ctypes.c_int, [_i32, _i64, _i64, _u32, _u32, _u32, _u64, _vp, _up]),
     "lw_hash_values": (ctypes.c_int, [_vp, _i64, _u64, _i32, _vp, _up]),
     "lw_uniform_keys": (ctypes.c_int, [_i64, _i64, _i64, _u64, _vp, _up]),
+    "lw_csr_permute": (ctypes.c_int, [_csr_p, _vp, _vp, _vp, _vp, _vp, _up]),
 }
 
 

@@ -27,6 +27,8 @@
 
 namespace lw {
 
+int sm_count();
+
 constexpr int HX_BINS = 1 << 16;
 constexpr int HX_MAX_HOT = 32768;   // sorted in one CTA's shared memory (128 KB)
 
@@ -98,13 +100,59 @@ __global__ void k_hx_remap(const int32_t* __restrict__ col, int64_t nnz,
     }
 }
 
+// ---- symmetric permutation P A P^T (degree relabeling for the iterated SpMV) ----
+// Row i' of the result is row order[i'] of A with every column c renamed
+// rank[c] (rank = order^-1); a row's atoms keep their order, so each row sum
+// adds the same products in the same sequence. One warp per output row, lanes
+// striding the row (coalesced on both sides); rows of any length.
+template <class OffT, class ValT>
+__global__ void k_csr_permute(const OffT* __restrict__ off, const int32_t* __restrict__ col,
+                              const ValT* __restrict__ val, const int64_t* __restrict__ order,
+                              const int32_t* __restrict__ rank, const OffT* __restrict__ off_out,
+                              int64_t rows, int32_t* __restrict__ col_out, ValT* __restrict__ val_out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += warps) {
+        const int64_t src = order[r];
+        const int64_t a0 = (int64_t)off[src], len = (int64_t)off[src + 1] - a0, b0 = (int64_t)off_out[r];
+        for (int64_t k = lane; k < len; k += 32) {
+            col_out[b0 + k] = rank[col[a0 + k]];
+            val_out[b0 + k] = val[a0 + k];
+        }
+    }
+}
+
+int csr_permute(const lw_csr_t* A, const int64_t* order, const int32_t* rank, const void* off_out,
+                int32_t* col_out, void* val_out, cudaStream_t s) {
+    if (!A || A->rows != A->cols || (A->rows > 0 && (!order || !rank || !off_out)) ||
+        (A->nnz > 0 && (!col_out || !val_out)))
+        return LW_E_INVALID_ARG;
+    if (A->rows == 0) return LW_OK;
+    const unsigned grid = (unsigned)sm_count() * 8;
+    if (A->offset_bits == 32) {
+        if (A->dtype == LW_F32)
+            k_csr_permute<int32_t, float><<<grid, 256, 0, s>>>((const int32_t*)A->row_offsets, A->col_indices,
+                (const float*)A->values, order, rank, (const int32_t*)off_out, A->rows, col_out, (float*)val_out);
+        else
+            k_csr_permute<int32_t, double><<<grid, 256, 0, s>>>((const int32_t*)A->row_offsets, A->col_indices,
+                (const double*)A->values, order, rank, (const int32_t*)off_out, A->rows, col_out, (double*)val_out);
+    } else {
+        if (A->dtype == LW_F32)
+            k_csr_permute<int64_t, float><<<grid, 256, 0, s>>>((const int64_t*)A->row_offsets, A->col_indices,
+                (const float*)A->values, order, rank, (const int64_t*)off_out, A->rows, col_out, (float*)val_out);
+        else
+            k_csr_permute<int64_t, double><<<grid, 256, 0, s>>>((const int64_t*)A->row_offsets, A->col_indices,
+                (const double*)A->values, order, rank, (const int64_t*)off_out, A->rows, col_out, (double*)val_out);
+    }
+    LW_LAUNCH_CHECK();
+    return LW_OK;
+}
+
 static size_t hx_align(size_t v) { return (v + 255) / 256 * 256; }
 
 size_t hotx_build_workspace(int64_t cols) {
     return hx_align((size_t)cols * 4) + hx_align((size_t)HX_BINS * 4) + 256;
 }
-
-int sm_count();
 
 int hotx_build(const lw_csr_t* A, int32_t max_hot, int32_t* col_packed, int32_t* hot_cols,
                int32_t* n_hot_out, void* ws, size_t ws_bytes, cudaStream_t s) {

@@ -31,6 +31,7 @@ size_t wo_hotx_workspace(int64_t rows, int64_t nnz, int64_t lanes, int64_t n_hot
 int spmv_work_oriented_hotx(const lw_csr_t*, const int32_t*, int32_t, const void*, void*, int64_t, void*,
                             size_t, unsigned, cudaStream_t);
 size_t hotx_build_workspace(int64_t cols);
+int csr_permute(const lw_csr_t*, const int64_t*, const int32_t*, const void*, int32_t*, void*, cudaStream_t);
 int hotx_build(const lw_csr_t*, int32_t, int32_t*, int32_t*, int32_t*, void*, size_t, cudaStream_t);
 int frontier_compact(const uint8_t*, int64_t, int32_t*, int64_t*, void*, cudaStream_t);
 int sssp_pass(const lw_csr_t*, const int32_t*, int64_t, double*, uint8_t*, int, int64_t, int64_t, int64_t, void*, cudaStream_t);
@@ -197,6 +198,13 @@ int lw_spmv_work_oriented_peers_hotx(const lw_csr_t* A, const int32_t* hot_cols,
     static const int32_t none = 0;   // selects the packed kernel even with no hot slots
     return spmv_work_oriented_peers(A, x, y, lanes, ws, ws_bytes, n_peers, peer_ptrs, multicast_ptr,
                                     row_base, (cudaStream_t)stream, hot_cols ? hot_cols : &none, n_hot);
+}
+
+int lw_csr_permute(const lw_csr_t* A, const int64_t* order, const int32_t* rank, const void* off_out,
+                   int32_t* col_out, void* val_out, uintptr_t stream) {
+    int rc = check_csr(A);
+    if (rc) return rc;
+    return csr_permute(A, order, rank, off_out, col_out, val_out, (cudaStream_t)stream);
 }
 
 size_t lw_hotx_build_workspace(int64_t cols) { return cols < 0 ? 0 : hotx_build_workspace(cols); }

@@ -39,9 +39,27 @@ __global__ void __launch_bounds__(VO_NT) k_sumsq_partials(const ValT* __restrict
     const int64_t b0 = (int64_t)blockIdx.x * VO_ITEMS;
     const int64_t b1 = min(b0 + VO_ITEMS, n);
     double acc = 0.0;
-    for (int64_t i = b0 + threadIdx.x; i < b1; i += VO_NT) {
-        const double v = (double)__ldg(y + i);
-        acc = fma(v, v, acc);
+    constexpr int V = 16 / sizeof(ValT);                   // elements per 16-byte vector
+    constexpr int PER = VO_ITEMS / VO_NT;                   // elements per thread (16)
+    using Vec = typename std::conditional<sizeof(ValT) == 4, float4, double2>::type;
+    if (b1 - b0 == VO_ITEMS && (uintptr_t)(y + b0) % 16 == 0) {
+        // full segment: all PER/V vector loads in flight before the first FMA,
+        // then a fixed accumulation order (run-to-run identical)
+        const Vec* yv = reinterpret_cast<const Vec*>(y + b0);
+        Vec r[PER / V];
+#pragma unroll
+        for (int h = 0; h < PER / V; ++h) r[h] = __ldg(yv + threadIdx.x + h * VO_NT);
+#pragma unroll
+        for (int h = 0; h < PER / V; ++h) {
+            const ValT* e = reinterpret_cast<const ValT*>(&r[h]);
+#pragma unroll
+            for (int k = 0; k < V; ++k) acc = fma((double)e[k], (double)e[k], acc);
+        }
+    } else {
+        for (int64_t i = b0 + threadIdx.x; i < b1; i += VO_NT) {
+            const double v = (double)__ldg(y + i);
+            acc = fma(v, v, acc);
+        }
     }
     const double t = block_sum(acc, s_w);
     if (threadIdx.x == 0) partials[blockIdx.x] = t;
@@ -57,8 +75,8 @@ __global__ void __launch_bounds__(VO_NT) k_sumsq_final(const double* __restrict_
 }
 
 template <class ValT>
-__global__ void k_scale(const ValT* __restrict__ y, int64_t n, const double* __restrict__ norm,
-                        ValT* __restrict__ x) {
+__global__ void k_scale(const ValT* y, int64_t n, const double* __restrict__ norm,
+                        ValT* x) {   // x may be y (in-place scaling)
     const double nrm = norm[0];
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
@@ -71,8 +89,8 @@ __global__ void k_scale(const ValT* __restrict__ y, int64_t n, const double* __r
 // independent divisions per thread keep the loads in flight (the scalar loop
 // serialises load -> fp64 divide -> store). Results are identical.
 template <class ValT>
-__global__ void k_scale_vec(const ValT* __restrict__ y, int64_t n, const double* __restrict__ norm,
-                            ValT* __restrict__ x) {
+__global__ void k_scale_vec(const ValT* y, int64_t n, const double* __restrict__ norm,
+                            ValT* x) {   // x may be y
     constexpr int V = 16 / sizeof(ValT);
     using Vec = typename std::conditional<sizeof(ValT) == 4, float4, double2>::type;
     const double nrm = norm[0];

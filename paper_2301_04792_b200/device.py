@@ -228,6 +228,37 @@ class DeviceCsr:
         self.__dict__["_hotx"] = hx
         return hx
 
+    def degree_relabel(self) -> "Relabeled":
+        """Symmetric degree relabeling P A P^T (one-time inspector for the
+        iterated SpMV, C5): vertices renumbered by decreasing in-degree (column
+        count; ties by index), so the most gathered x entries form a dense
+        prefix of x' = P x that stays in L2/L1, and the rows follow the same
+        renumbering so y' = P y feeds the next iteration directly. Each row keeps
+        its atoms in order: its products and their sequence are unchanged. The
+        caller iterates on ``.matrix`` from ``P x0`` (``.to_new``) and maps the
+        result back once (``.to_old``). Square matrices only."""
+        torch = _torch()
+        if self.rows != self.cols:
+            raise ValueError("degree_relabel needs a square matrix")
+        n = self.rows
+        counts = torch.bincount(self.col_indices.to(torch.int64), minlength=n) if self.nnz else \
+            torch.zeros(n, dtype=torch.int64, device=self.device)
+        order = torch.sort(counts, descending=True, stable=True).indices      # new -> old
+        rank = torch.empty(n, dtype=torch.int32, device=self.device)
+        rank[order] = torch.arange(n, dtype=torch.int32, device=self.device)  # old -> new
+        lengths = (self.row_offsets[1:] - self.row_offsets[:-1]).to(torch.int64)[order]
+        off = torch.zeros(n + 1, dtype=torch.int64, device=self.device)
+        torch.cumsum(lengths, 0, out=off[1:])
+        off = off.to(self.row_offsets.dtype)
+        col = torch.empty_like(self.col_indices)
+        val = torch.empty_like(self.values)
+        lib = _lib.load()
+        _lib.check(lib.lw_csr_permute(self.c_struct(), order.data_ptr(), rank.data_ptr(), off.data_ptr(),
+                                      col.data_ptr() if self.nnz else None,
+                                      val.data_ptr() if self.nnz else None, current_stream(self.device)),
+                   "lw_csr_permute")
+        return Relabeled(DeviceCsr(n, n, off, col, val), order, rank)
+
     def hot_columns(self) -> "HotColumns | None":
         """The hot-x packing built by pack_hot_columns, if the tensors are unchanged."""
         hx = self.__dict__.get("_hotx")
@@ -349,6 +380,24 @@ class Probe:
                 "atom_lane": self.atom_lane[: self.nnz].cpu().numpy(),
                 "atom_tile": self.atom_tile[: self.nnz].cpu().numpy(),
                 "atom_visits": self.atom_visits[: self.nnz].cpu().numpy()}
+
+
+@dataclass
+class Relabeled:
+    """A symmetric relabeling P A P^T: ``matrix`` is the permuted operator,
+    ``order[i']`` the original index of new vertex i', ``rank`` its inverse."""
+
+    matrix: DeviceCsr
+    order: object
+    rank: object
+
+    def to_new(self, v):
+        """P v: original numbering -> relabeled (v'[i'] = v[order[i']])."""
+        return v.index_select(0, self.order)
+
+    def to_old(self, v):
+        """P^T v': relabeled numbering -> original (v[i] = v'[rank[i]])."""
+        return v.index_select(0, self.rank.to(self.order.dtype))
 
 
 @dataclass

@@ -15,7 +15,8 @@ from __future__ import annotations
 import numpy as np
 
 __all__ = ["nnz_balanced_bounds", "shard_of", "power_iteration", "power_iteration_fused",
-           "power_iteration_graph", "chunk_bounds", "RowShard"]
+           "power_iteration_graph", "power_iteration_inplace", "chunk_bounds", "RowShard",
+           "GatherLayout"]
 
 
 def nnz_balanced_bounds(row_offsets, parts: int) -> np.ndarray:
@@ -68,6 +69,154 @@ def chunk_bounds(rows: int, chunks: int) -> np.ndarray:
     """Split local rows [0, rows) into ``chunks`` contiguous, near-equal pieces."""
     chunks = max(1, int(chunks))
     return (np.arange(chunks + 1, dtype=np.int64) * rows) // chunks
+
+
+class GatherLayout:
+    """Where each row of the full vector sits in the all-gather buffer.
+
+    The shards' row counts are uneven (nnz-balanced bounds), NCCL's all-gather
+    moves equal slots, so slot (chunk k, rank r) holds width_k = max_r(rows of
+    chunk k of rank r) entries: the buffer is chunk-major, rank-major, with
+    zero padding after each slot's real rows. ``pos[i]`` is the buffer index of
+    global row i. Renaming the operator's columns through ``pos`` once
+    (``remap_columns``) lets every iteration read x straight out of the
+    gathered buffer: the SpMV writes its rows into its own slot, NCCL gathers
+    in place, the norm and the scaling run over the buffer (padding stays 0) —
+    no send copy, concatenation or reorder pass per iteration."""
+
+    def __init__(self, bounds, chunks: int = 1):
+        b = np.asarray(bounds, dtype=np.int64)
+        self.world = b.size - 1
+        self.chunks = max(1, int(chunks))
+        counts = np.diff(b)
+        self.cb = [chunk_bounds(int(c), self.chunks) for c in counts]
+        self.widths = [max(int(self.cb[r][k + 1] - self.cb[r][k]) for r in range(self.world))
+                       for k in range(self.chunks)]
+        self.offs = np.concatenate([[0], np.cumsum([self.world * w for w in self.widths])]).astype(np.int64)
+        self.size = int(self.offs[-1])
+        pos = np.empty(int(b[-1]), dtype=np.int64)
+        for r in range(self.world):
+            for k in range(self.chunks):
+                lo, hi = int(b[r] + self.cb[r][k]), int(b[r] + self.cb[r][k + 1])
+                base = int(self.offs[k] + r * self.widths[k])
+                pos[lo:hi] = base + np.arange(hi - lo)
+        self.pos = pos
+        self._pos_dev = {}
+
+    def pos_on(self, device):
+        """``pos`` as an int64 tensor on ``device`` (uploaded once per device)."""
+        import torch
+
+        key = str(device)
+        if key not in self._pos_dev:
+            self._pos_dev[key] = torch.as_tensor(self.pos, device=device)
+        return self._pos_dev[key]
+
+    def slot(self, rank: int, k: int) -> tuple[int, int, int, int]:
+        """(buffer start of my slot, slot width, local row range r0, r1) of chunk k."""
+        return (int(self.offs[k] + rank * self.widths[k]), self.widths[k],
+                int(self.cb[rank][k]), int(self.cb[rank][k + 1]))
+
+    def remap_columns(self, m):
+        """The operator with column c renamed pos[c] (host CsrMatrix or DeviceCsr);
+        its column count becomes the buffer size."""
+        from .sparse import CsrMatrix
+
+        if isinstance(m, CsrMatrix):
+            return CsrMatrix(m.rows, self.size, m.row_offsets, self.pos[m.col_indices], m.values)
+        import torch
+
+        from .device import DeviceCsr
+
+        pos = torch.as_tensor(self.pos.astype(np.int32), device=m.device)
+        col = pos.index_select(0, m.col_indices.to(torch.int64)) if m.nnz else m.col_indices.clone()
+        return DeviceCsr(m.rows, self.size, m.row_offsets, col, m.values)
+
+    def to_layout(self, x):
+        """Full vector -> buffer form (zeros in the padding)."""
+        import torch
+
+        out = torch.zeros(self.size, dtype=x.dtype, device=x.device)
+        out[self.pos_on(x.device)] = x
+        return out
+
+    def from_layout(self, buf):
+        return buf.index_select(0, self.pos_on(buf.device))
+
+
+def power_iteration_inplace(local_spmv, layout: GatherLayout, iters: int, rank: int = 0, group=None,
+                            x0=None, dtype=None, device=None, _norms_out=None):
+    """power_iteration over a GatherLayout: x lives in the gather buffer form.
+
+    ``local_spmv(x_buf, r0, r1, out)`` writes this rank's local rows [r0, r1)
+    (operator columns remapped with ``layout.remap_columns``) into ``out``, a
+    view of this rank's slot. Per iteration and chunk k: the SpMV writes the
+    slot, an async NCCL all-gather fills chunk k of the next buffer in place
+    (overlapping chunk k+1's SpMV); then one norm read and one in-place scaling
+    of the buffer. Two buffers alternate (x_k is read while x_{k+1} is
+    gathered). Returns (x in buffer form, norms); ``layout.from_layout`` maps it
+    back once."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world != layout.world:
+        raise ValueError(f"layout built for {layout.world} ranks, group has {world}")
+    dt = dtype or torch.float32
+    bufs = [torch.zeros(layout.size, dtype=dt, device=device) for _ in range(2)]
+    if x0 is None:
+        n = layout.pos.size
+        bufs[0].copy_(layout.to_layout(torch.full((n,), 1.0 / np.sqrt(n), dtype=dt, device=device)))
+    else:
+        bufs[0].copy_(x0)
+    norms = []
+    cur = 0
+    for it in range(iters):
+        x, nxt = bufs[cur], bufs[1 - cur]
+        works = []
+        for k in range(layout.chunks):
+            start, width, r0, r1 = layout.slot(rank, k)
+            local_spmv(x, r0, r1, nxt[start:start + (r1 - r0)])
+            if world > 1:
+                lo, hi = int(layout.offs[k]), int(layout.offs[k + 1])
+                works.append(dist.all_gather_into_tensor(nxt[lo:hi], nxt[start:start + width],
+                                                         group=group, async_op=True))
+        for w in works:
+            w.wait()
+        nrm = _normalise_into(nxt)
+        if _norms_out is not None:
+            _norms_out[it].copy_(nrm)
+        else:
+            norms.append(nrm)
+        cur = 1 - cur
+    if _norms_out is not None:
+        return bufs[cur], None
+    return bufs[cur], [float(v) for v in norms]
+
+
+def _normalise_into(y):
+    """||y||_2 (device fp64 scalar) and y /= ||y|| in place (library kernels on
+    CUDA; torch on CPU for the gloo tests)."""
+    import torch
+
+    if not y.is_cuda:
+        nrm = torch.linalg.vector_norm(y, dtype=torch.float64)
+        if nrm > 0:
+            y.copy_((y / nrm).to(y.dtype))
+        return nrm
+    from . import _lib
+    from .device import _dtype_code, current_stream
+
+    lib = _lib.load()
+    code = _dtype_code(y.dtype)
+    stream = current_stream(y.device)
+    ws = _NORM_WS.get(max(lib.lw_norm_workspace(y.numel()), 8), y.device, stream)
+    nrm = torch.empty((), dtype=torch.float64, device=y.device)
+    _lib.check(lib.lw_vector_norm(y.data_ptr(), y.numel(), code, ws.data_ptr(), ws.numel(),
+                                  nrm.data_ptr(), stream), "lw_vector_norm")
+    _lib.check(lib.lw_vector_scale(y.data_ptr(), y.numel(), code, nrm.data_ptr(), y.data_ptr(),
+                                   stream), "lw_vector_scale")
+    return nrm
 
 
 def power_iteration_graph(local_spmv, n: int, shard: RowShard, iters: int, group=None,

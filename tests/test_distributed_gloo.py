@@ -121,3 +121,66 @@ def test_chunked_single_process_equals_plain():
     # the per-chunk SpMV cuts rows differently (merge-path lanes), so only FP order differs
     np.testing.assert_allclose(x4.numpy(), x1.numpy(), rtol=1e-12, atol=1e-15)
     np.testing.assert_allclose(n4, n1, rtol=1e-12)
+
+
+def _worker_inplace(rank, world, port, out, chunks):
+    """The in-place gather layout: operator columns renamed into the gather
+    buffer, SpMV writing its slot, all-gather in place, norm + scale in place."""
+    from oracle import oracle
+    from paper_2301_04792_b200.distributed import GatherLayout, power_iteration_inplace
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m = lw.generate_power_law_csr(4000, 10.0, 1.2, seed=7)
+        b = nnz_balanced_bounds(m.row_offsets, world)
+        lay = GatherLayout(b, chunks)
+        mine = lay.remap_columns(shard_of(m, b, rank))
+
+        def local(x, r0, r1, out_view):
+            part = shard_of(mine, [0, r0, r1], 1)
+            out_view.copy_(torch.from_numpy(oracle.spmv(part.row_offsets, part.col_indices, part.values,
+                                                        x.double().numpy(), "merge-path", lanes=32)))
+
+        xb, norms = power_iteration_inplace(local, lay, 8, rank=rank, dtype=torch.float64)
+        out[rank] = (lay.from_layout(xb).numpy().copy(), list(norms))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,chunks", [(2, 1), (2, 3), (3, 2)])
+def test_inplace_gather_layout_matches_single_process(world, chunks):
+    from oracle import oracle
+
+    port = _free_port()
+    mgr = mp.get_context("spawn").Manager()
+    out = mgr.dict()
+    mp.start_processes(_worker_inplace, args=(world, port, out, chunks), nprocs=world, join=True,
+                       start_method="spawn")
+    m = lw.generate_power_law_csr(4000, 10.0, 1.2, seed=7)
+    x = np.full(m.rows, 1.0 / np.sqrt(m.rows))
+    norms = []
+    for _ in range(8):
+        y = oracle.spmv(m.row_offsets, m.col_indices, m.values, x, "merge-path", lanes=32)
+        norms.append(np.linalg.norm(y))
+        x = y / norms[-1]
+    for r in range(world):
+        xr, nr = out[r]
+        np.testing.assert_allclose(xr, x, rtol=1e-10, atol=1e-13)
+        np.testing.assert_allclose(nr, norms, rtol=1e-12)
+    np.testing.assert_array_equal(out[0][0], out[world - 1][0])
+
+
+def test_gather_layout_positions():
+    from paper_2301_04792_b200.distributed import GatherLayout
+
+    b = np.array([0, 5, 12, 13])
+    lay = GatherLayout(b, chunks=2)
+    # slots: chunk 0 widths max(2, 3, 0)=3, chunk 1 max(3, 4, 1)=4 -> size 3*3 + 3*4
+    assert lay.widths == [3, 4] and lay.size == 21
+    assert sorted(lay.pos.tolist()) == sorted(set(lay.pos.tolist()))   # injective
+    v = torch.arange(13, dtype=torch.float64)
+    np.testing.assert_array_equal(lay.from_layout(lay.to_layout(v)).numpy(), v.numpy())
+    buf = lay.to_layout(v)
+    pad = np.setdiff1d(np.arange(lay.size), lay.pos)
+    assert (buf[torch.as_tensor(pad)] == 0).all()

@@ -193,3 +193,55 @@ def test_c5_power_iteration_rmat26_per_iterate(hot):
         assert worst <= 1.0, f"iterate {k + 1}: worst err/bound {worst:.3g}"
     del A
     torch.cuda.empty_cache()
+
+
+def test_c5_relabeled_inplace_driver_per_iterate():
+    """The bench's C5 path: degree-relabeled operator P A P^T (+ hot-x), the
+    in-place gather-layout driver, iterates mapped back to the original
+    numbering and checked against the oracle on the ORIGINAL matrix."""
+    from paper_2301_04792_b200.distributed import GatherLayout, power_iteration_inplace
+
+    _cache.clear()
+    torch.cuda.empty_cache()
+    A = lwb.generate_rmat_csr(26, 16, seed=5, dtype="float32")
+    host = [t.cpu().numpy() for t in (A.row_offsets, A.col_indices, A.values)]
+    R = A.degree_relabel()
+    n = A.rows
+    del A
+    lay = GatherLayout(np.array([0, n]), 1)
+    M = lay.remap_columns(R.matrix)
+    M.pack_hot_columns()
+    cfg = ExecutorConfig(schedule=K.WORK_ORIENTED)
+
+    def local(x, r0, r1, out):
+        lwb.spmv(M, x, cfg, out=out)
+
+    x = torch.full((n,), 1.0 / np.sqrt(n), dtype=torch.float32, device="cuda")
+    for k in range(3):
+        xk = x.cpu().numpy()
+        xb, norms = power_iteration_inplace(local, lay, 1, x0=lay.to_layout(R.to_new(x)),
+                                            dtype=torch.float32, device="cuda")
+        x = R.to_old(lay.from_layout(xb))
+        y_ref, scale = oracle.spmv_narrow(*host, xk)
+        nrm = float(np.linalg.norm(y_ref))
+        assert abs(norms[-1] - nrm) <= 1e-5 * float(np.linalg.norm(scale)), (k, norms[-1], nrm)
+        bound = 1e-5 * (scale + np.abs(y_ref)) / nrm
+        err = np.abs(x.cpu().numpy().astype(np.float64) - y_ref / nrm)
+        worst = float((err / np.maximum(bound, 1e-300)).max())
+        assert worst <= 1.0, f"iterate {k + 1}: worst err/bound {worst:.3g}"
+
+
+def test_degree_relabel_keeps_row_sums():
+    """P A P^T: row i' of the relabeled matrix is row order[i'] with renamed
+    columns and the atoms in their original order, so y' = P y bit for bit
+    (integer data: exact in any summation order, so bit-equal)."""
+    A = lwb.generate_rmat_csr(18, 16, seed=2, dtype="float64")
+    A.values.copy_(torch.randint(-4, 5, (A.nnz,), device="cuda").to(torch.float64))   # exact sums
+    R = A.degree_relabel()
+    x = torch.randint(-3, 4, (A.cols,), device="cuda").to(torch.float64)
+    tm = ExecutorConfig(schedule=K.THREAD_MAPPED)
+    y = lwb.spmv(A, x, tm)
+    yr = lwb.spmv(R.matrix, R.to_new(x), tm)
+    assert torch.equal(R.to_old(yr), y)
+    counts = torch.bincount(R.matrix.col_indices.long(), minlength=A.cols)
+    assert bool((counts[:-1] >= counts[1:]).all())   # columns by decreasing degree
