@@ -293,14 +293,53 @@ __global__ void __launch_bounds__(256, LW_GW_MINB)
 }
 
 // ---- block tiles ------------------------------------------------------------------
-template <class OffT, class ValT, int NT, bool PROBE>
-__global__ void __launch_bounds__(NT)
+// Block selection of the uninstrumented block-tile SpMV: a block is STAGED when
+// all its rows have <= GB_LONG atoms and either none exceeds GB_LONG/4 or at
+// least a quarter do (no lone long row for one thread to sum while the CTA
+// waits at the barrier); the other blocks run the cooperative path. Unlike the
+// warp tiles (two launches), both paths live in one kernel and share one
+// shared-memory buffer: as two launches the staged launch's time adds to the
+// cooperative launch's tail on power-law inputs (C4 skew 1.05 fp32 1.22 ->
+// 1.57 ms), in one grid the short blocks fill in under the long ones.
+#ifndef LW_GB_LONG
+#define LW_GB_LONG 64
+#endif
+#ifndef LW_GB_CAP      // atoms per staged segment (fp32 products; fp64 holds half)
+#define LW_GB_CAP 4096
+#endif
+#ifndef LW_GB_SU       // member-stride steps of loads in flight on the staged path
+#define LW_GB_SU 4
+#endif
+constexpr int GB_LONG = LW_GB_LONG, GB_SU = LW_GB_SU;
+constexpr int GB_ALL = 0, GB_FUSED = 1;
+
+template <class OffT>
+__device__ __forceinline__ bool gb_staged_block(OffT cnt, int tc, int NT_) {
+    // block max and sum of the row lengths (every thread of the CTA calls this)
+    const bool too_long = __syncthreads_or(cnt > (OffT)GB_LONG);
+    if (too_long) return false;
+    const int n_ge = __syncthreads_count(cnt * 4 > (OffT)GB_LONG);   // rows above a quarter of the limit
+    (void)NT_;
+    // mostly-short blocks with a few long rows would serialise on those rows
+    return n_ge == 0 || n_ge * 4 >= tc || tc < 8;
+}
+
+#ifndef LW_GB_MINB   // resident CTAs the fused kernel's registers must allow (A/B; 1 = free)
+#define LW_GB_MINB 1
+#endif
+template <class OffT, class ValT, int NT, bool PROBE, int MODE = GB_ALL>
+__global__ void __launch_bounds__(NT, MODE == GB_FUSED ? LW_GB_MINB * 256 / NT : 1)
     k_group_block(Csr<OffT, ValT> A, const ValT* __restrict__ x, ValT* __restrict__ y,
                   int64_t groups, Probe probe) {
     constexpr int NW = NT / kWarp;
+    constexpr int CAP = (MODE == GB_FUSED && LW_GB_CAP > 0) ? LW_GB_CAP * 4 / (int)sizeof(ValT) : 1;
+    constexpr size_t RAW = sizeof(double) * NW * NT > sizeof(ValT) * CAP ? sizeof(double) * NW * NT
+                                                                          : sizeof(ValT) * CAP;
     __shared__ OffT s_excl[NT + 1];
     __shared__ OffT s_wsum[NW];
-    __shared__ double s_acc[NW][NT];
+    __shared__ __align__(16) unsigned char s_raw[RAW];   // cooperative accumulators | staged products
+    double(*s_acc)[NT] = reinterpret_cast<double(*)[NT]>(s_raw);
+    ValT* s_prod = reinterpret_cast<ValT*>(s_raw);
     const int tid = threadIdx.x, lane = tid & (kWarp - 1), warp = tid >> 5;
     const int64_t nblocks = (A.rows + NT - 1) / NT;
     const int64_t glane = (int64_t)blockIdx.x * NT + tid;
@@ -309,6 +348,65 @@ __global__ void __launch_bounds__(NT)
         const int64_t tb = b * NT;
         const int tc = (int)min((int64_t)NT, A.rows - tb);
         const OffT cnt = tid < tc ? A.off[tb + tid + 1] - A.off[tb + tid] : (OffT)0;
+        bool staged = false;
+        if constexpr (MODE == GB_FUSED) staged = gb_staged_block<OffT>(cnt, tc, NT);
+        if (staged) {
+            // Staged block: the members compute their atoms' products exactly as
+            // the schedule assigns them (member m: block-local atoms m, m+NT, ...;
+            // GB_SU steps of loads in flight) into shared memory, one tile-aligned
+            // segment of <= CAP atoms at a time; the thread owning tile t then sums
+            // the tile's products in atom order (fp64) and writes y once. No per-atom
+            // get_tile search, no per-step segmented reduction.
+            OffT incl = cnt;
+#pragma unroll
+            for (int d = 1; d < kWarp; d <<= 1) {
+                const OffT o = shfl_up(incl, d);
+                if (lane >= d) incl += o;
+            }
+            if (lane == kWarp - 1) s_wsum[warp] = incl;
+            __syncthreads();
+            OffT wpre = 0;
+            for (int w = 0; w < warp; ++w) wpre += s_wsum[w];
+            incl += wpre;
+            const OffT excl = incl - cnt;
+            s_excl[tid] = excl;
+            if (tid == NT - 1) s_excl[NT] = incl;
+            const int64_t base = (int64_t)A.off[tb];
+            __syncthreads();
+            int ta = 0;
+            while (ta < tc) {
+                const OffT sa = s_excl[ta];
+                // tiles ta .. te-1 whose atoms end within sa + CAP (incl increases)
+                const int te = ta + __syncthreads_count(tid >= ta && tid < tc && incl - sa <= (OffT)CAP);
+                const OffT sb = s_excl[te];
+                for (OffT k0 = sa - sa % (OffT)NT; k0 < sb; k0 += GB_SU * NT) {
+                    int32_t c[GB_SU];
+                    ValT v[GB_SU];
+#pragma unroll
+                    for (int u = 0; u < GB_SU; ++u) {
+                        const OffT k = k0 + u * NT + tid;
+                        const bool valid = k >= sa && k < sb;
+                        c[u] = valid ? ld_stream(A.col + base + k) : 0;
+                        v[u] = valid ? ld_stream(A.val + base + k) : (ValT)0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < GB_SU; ++u) {
+                        const OffT k = k0 + u * NT + tid;
+                        if (k >= sa && k < sb) s_prod[k - sa] = v[u] * ld_gather(x + c[u]);
+                    }
+                }
+                __syncthreads();
+                if (tid >= ta && tid < te) {
+                    double acc = 0.0;
+                    const int e0 = (int)(excl - sa), n = (int)cnt;
+                    for (int j = 0; j < n; ++j) acc += (double)s_prod[e0 + j];
+                    y[tb + tid] = (ValT)acc;
+                }
+                __syncthreads();
+                ta = te;
+            }
+            continue;
+        }
         // block exclusive scan of the counts
         OffT incl = cnt;
 #pragma unroll
@@ -442,14 +540,12 @@ static int64_t groups_per_sm(int64_t gs, int64_t tpb) {
                 resident_ctas(k_group_warp<int32_t, float, false, (LW_GW_CAP > 0 ? GW_STAGED : GW_ALL)>, 256),
                 resident_ctas(k_group_warp<int32_t, float, false, (LW_GW_CAP > 0 ? GW_COOP : GW_ALL)>, 256)) * 8;
             if (w > 0) return w;
-        } else if (gs == tpb && gs == 256) {
-            static const int64_t b = resident_ctas(k_group_block<int32_t, float, 256, false>, 256);
-            if (b > 0) return b;
-        } else if (gs == tpb && gs == 128) {
-            static const int64_t b = resident_ctas(k_group_block<int32_t, float, 128, false>, 128);
-            if (b > 0) return b;
-        } else if (gs == tpb && gs == 64) {
-            static const int64_t b = resident_ctas(k_group_block<int32_t, float, 64, false>, 64);
+        } else if (gs == tpb && (gs == 256 || gs == 128 || gs == 64)) {
+            // one resident wave of the launched (fused) kernel
+#define LW_GB_OCC(NT) resident_ctas(k_group_block<int32_t, float, NT, false, (LW_GB_CAP > 0 ? GB_FUSED : GB_ALL)>, NT)
+            static const int64_t b256 = LW_GB_OCC(256), b128 = LW_GB_OCC(128), b64 = LW_GB_OCC(64);
+#undef LW_GB_OCC
+            const int64_t b = gs == 256 ? b256 : gs == 128 ? b128 : b64;
             if (b > 0) return b;
         }
     }
@@ -496,8 +592,13 @@ static int launch_group(const lw_csr_t* A, const void* x, void* y, int64_t lanes
             const int64_t groups = lanes / gs;
 #define LW_GB(NT)                                                                           \
     if (gs == NT) {                                                                         \
-        if (probe) k_group_block<OffT, ValT, NT, true><<<groups, NT, 0, s>>>(a, xv, yv, groups, p); \
-        else       k_group_block<OffT, ValT, NT, false><<<groups, NT, 0, s>>>(a, xv, yv, groups, p); \
+        if (probe) {                                                                        \
+            k_group_block<OffT, ValT, NT, true><<<groups, NT, 0, s>>>(a, xv, yv, groups, p); \
+        } else if (LW_GB_CAP > 0) {                                                         \
+            k_group_block<OffT, ValT, NT, false, GB_FUSED><<<groups, NT, 0, s>>>(a, xv, yv, groups, p); \
+        } else {                                                                            \
+            k_group_block<OffT, ValT, NT, false><<<groups, NT, 0, s>>>(a, xv, yv, groups, p); \
+        }                                                                                   \
     }
             LW_GB(64) LW_GB(128) LW_GB(256)
 #undef LW_GB

@@ -4,5 +4,5 @@ import sys,json
 for l in sys.stdin:
     try: r=json.loads(l)
     except Exception: continue
-    if r['schedule'] in ('${SCHED:-group_warp}',): print(r['config'], r['matrix'][:34], r['dtype'], r['schedule'], r['ms'])
+    if r['schedule'] in ('${SCHED:-group_warp}',): print(r['config'], r['matrix'][:48], r['dtype'], r['schedule'], r['ms'])
 "; done

@@ -51,8 +51,9 @@ def matrices(names):
             d = lwb.generate_banded_device(1_000_000, 16, seed=2)
             yield "C2b", "banded 1M rows, half-bandwidth 16", d, d.row_offsets.cpu().numpy()
         elif name == "C2u":
-            m = lwb.generate_random_csr(1_000_000, 1_000_000, 32_000_000, seed=2)
-            yield "C2u", "random 1M x 1M, 32M nnz, seed 2", m.to_device("float32"), m.row_offsets
+            # device twin of generate_random_csr (the host generator takes minutes here)
+            d = lwb.generate_uniform_device(1_000_000, 1_000_000, 32_000_000, seed=2)
+            yield "C2u", "uniform 1M x 1M, 32M draws, seed 2 (device)", d, d.row_offsets.cpu().numpy()
         elif name == "C3":
             d = lwb.generate_rmat_csr(24, 16, seed=3)
             yield "C3", "R-MAT scale 24, ef 16, seed 3", d, d.row_offsets.cpu().numpy()
@@ -60,8 +61,8 @@ def matrices(names):
             for skew in (3.0, 2.0, 1.5, 1.2, 1.1, 1.05):
                 m = lwb.generate_power_law_csr(1 << 20, 16.0, skew, seed=4)
                 yield "C4", f"power-law 2^20 rows, avg 16, skew {skew}", m.to_device("float32"), m.row_offsets
-            m = lwb.generate_random_csr(1 << 20, 1 << 20, 16 << 20, seed=4)
-            yield "C4", "uniform 2^20 x 2^20, 16 nnz/row", m.to_device("float32"), m.row_offsets
+            d = lwb.generate_uniform_device(1 << 20, 1 << 20, 16 << 20, seed=4)
+            yield "C4", "uniform 2^20 x 2^20, 16 draws/row (device)", d, d.row_offsets.cpu().numpy()
             d = lwb.generate_banded_device(1 << 20, 8, seed=4)
             yield "C4", "banded 2^20 rows, half-bandwidth 8", d, d.row_offsets.cpu().numpy()
 
@@ -99,6 +100,7 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--dtypes", default="float32,float64")
+    ap.add_argument("--schedules", default="thread_mapped,work_oriented,group_warp,group_block")
     args = ap.parse_args()
     hbm = peak()
     threads = oracle.default_threads()
@@ -109,7 +111,7 @@ def main():
             A = A32 if dtype == "float32" else A32.astype("float64")
             x = torch.ones(A.cols, dtype=A.dtype, device=A.device)
             cold = A.algorithmic_bytes() < 256 << 20
-            for sname, kind, gs in SCHEDULES:
+            for sname, kind, gs in [s for s in SCHEDULES if s[0] in args.schedules.split(",")]:
                 cfg = lwb.ExecutorConfig(schedule=kind, group_size=gs)
                 ms, y = time_gpu(A, x, cfg, args.reps, cold)
                 gbs = A.algorithmic_bytes() / (ms * 1e-3) / 1e9
