@@ -47,13 +47,17 @@ struct WoCfg;
 #ifndef LW_WO_NT
 #define LW_WO_NT 512
 #endif
+// MAXR: register cap (fp64: 40 keeps 3 x 512 threads resident per SM; the
+// allocator otherwise lands at 46-58). fp32 is left uncapped: it lands at 32
+// (4 x 512, full occupancy) by itself, and a __maxnreg__(32) changes its code
+// generation for the worse (0.992 -> 1.005 ms packed on C3).
 template <>
 struct WoCfg<float> {
-    static constexpr int NT = LW_WO_NT, IPT = WO_W / LW_WO_NT;
+    static constexpr int NT = LW_WO_NT, IPT = WO_W / LW_WO_NT, MAXR = 0;   // uncapped
 };
 template <>
 struct WoCfg<double> {
-    static constexpr int NT = LW_WO_NT, IPT = WO_W / LW_WO_NT;
+    static constexpr int NT = LW_WO_NT, IPT = WO_W / LW_WO_NT, MAXR = 40;
 };
 
 // ---- 1. partition ---------------------------------------------------------
@@ -235,19 +239,33 @@ __device__ __forceinline__ void ld_atoms(const int32_t* col, const ValT* val, in
     }
 }
 
-// IPT consecutive values into shared memory with 16-byte stores (scalar stores
-// of a thread's consecutive slots would be an IPT-way bank conflict)
-template <int IPT>
-__device__ __forceinline__ void store_run(float* dst, const float* v) {
-    float4* d = reinterpret_cast<float4*>(dst);
+// fp64 running sums s_seg are stored transposed: window position pos lives at
+// (pos % IPT) * NT + pos / IPT, so thread t writes its IPT consecutive sums with
+// IPT scalar stores at t, NT + t, ... — every warp store is 32 consecutive
+// doubles, conflict-free. Row-major with 16-byte stores puts a quarter warp's 8
+// stores in 2 bank groups (53 M conflict wavefronts per C3 launch); transposed,
+// fp64 C3 goes 1.588 -> 1.478 ms. fp32 stays row-major with float4 stores: its
+// 2-way conflicts (9 M wavefronts) cost less than the 8 scalar stores
+// (1.005 -> 1.026 ms packed, DESIGN.md kernel log).
+template <class ValT>
+struct SegT {
+    static constexpr bool on = sizeof(ValT) == 8;
+};
+template <class ValT, int NT, int IPT>
+__device__ __forceinline__ int seg_at(int pos) {
+    if constexpr (!SegT<ValT>::on) return pos;
+    else return (int)(((unsigned)pos % IPT) * NT + (unsigned)pos / IPT);
+}
+template <int NT, int IPT>
+__device__ __forceinline__ void store_run(float* seg, int pos, const float* v) {
+    float4* d = reinterpret_cast<float4*>(seg + pos);
 #pragma unroll
     for (int h = 0; h < IPT / 4; ++h) d[h] = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
 }
-template <int IPT>
-__device__ __forceinline__ void store_run(double* dst, const double* v) {
-    double2* d = reinterpret_cast<double2*>(dst);
+template <int NT, int IPT>
+__device__ __forceinline__ void store_run(double* seg, int pos, const double* v) {
 #pragma unroll
-    for (int h = 0; h < IPT / 2; ++h) d[h] = make_double2(v[2 * h], v[2 * h + 1]);
+    for (int k = 0; k < IPT; ++k) seg[k * NT + (unsigned)pos / IPT] = v[k];
 }
 
 // Hot-x packed gather (lw_hotx_build relabels the most gathered columns c to
@@ -274,12 +292,11 @@ __device__ __forceinline__ double ld_hotx(const double* x, const double* xh, int
     return v;
 }
 
-template <class OffT, class ValT, bool PROBE, bool VEC, bool PEERS = false, bool HOT = false>
-__global__ void __launch_bounds__(WoCfg<ValT>::NT)
-    k_wo_chunk(Csr<OffT, ValT> A, const ValT* __restrict__ x, ValT* __restrict__ y,
-               int64_t items, int64_t J, const int64_t* __restrict__ bound_tile,
-               int64_t* __restrict__ carry_tile, double* __restrict__ carry_val, Probe probe,
-               PeerOut po = PeerOut{}, const ValT* __restrict__ xh = nullptr) {
+template <class OffT, class ValT, bool PROBE, bool VEC, bool PEERS, bool HOT>
+__device__ __forceinline__ void wo_chunk_body(Csr<OffT, ValT> A, const ValT* __restrict__ x, ValT* __restrict__ y,
+                                              int64_t items, int64_t J, const int64_t* __restrict__ bound_tile,
+                                              int64_t* __restrict__ carry_tile, double* __restrict__ carry_val,
+                                              Probe probe, PeerOut po, const ValT* __restrict__ xh) {
     constexpr int NT = WoCfg<ValT>::NT, IPT = WoCfg<ValT>::IPT;
     constexpr int W = WO_W, S = WO_S;
     static_assert(NT * IPT == W, "window must be NT*IPT atoms");
@@ -419,7 +436,7 @@ __global__ void __launch_bounds__(WoCfg<ValT>::NT)
                 r = ((fl >> k) & 1u) ? p[k] : r + p[k];
                 p[k] = r;
             }
-            store_run<IPT>(s_seg + pos, p);
+            store_run<NT, IPT>(s_seg, pos, p);
         }
         __syncthreads();
 
@@ -427,7 +444,7 @@ __global__ void __launch_bounds__(WoCfg<ValT>::NT)
         for (int i = tid; i < n_rows; i += NT) {
             const int e = s_end[i];
             const int st = i ? s_end[i - 1] : w0;
-            double v = e > st ? (double)s_seg[e - 1] : 0.0;
+            double v = e > st ? (double)s_seg[seg_at<ValT, NT, IPT>(e - 1)] : 0.0;
             if (i == 0 && run_has && run_row == t0) v += run_val;
             y[t0 + i] = (ValT)v;
             if (PEERS) peer_store<HOT>(po, s_peer, t0 + i, (ValT)v);   // smem bases: packed 1.24 -> 1.18 ms, unpacked 1.30 -> 1.50 (kept on the constant bank)
@@ -447,7 +464,7 @@ __global__ void __launch_bounds__(WoCfg<ValT>::NT)
         {
             const int st = n_rows ? s_end[n_rows - 1] : w0;
             const bool tail = w1 > st;
-            const double tv = tail ? (double)s_seg[w1 - 1] : 0.0;
+            const double tv = tail ? (double)s_seg[seg_at<ValT, NT, IPT>(w1 - 1)] : 0.0;
             if (n_rows > 0) {
                 run_row = t1; run_val = tv; run_has = tail;
             } else if (run_has && run_row == t1) {
@@ -464,6 +481,30 @@ __global__ void __launch_bounds__(WoCfg<ValT>::NT)
         carry_val[l] = live ? run_val : 0.0;
         if (PROBE && probe.lane_atoms) probe.lane_atoms[l] = lane_atoms;
     }
+}
+
+// The chunk kernel: fp32 with the allocator's own register choice (32), fp64
+// capped at WoCfg<double>::MAXR (40; the peers variant 48) — see WoCfg.
+#define LW_WO_PARAMS                                                                                  \
+    Csr<OffT, ValT> A, const ValT *__restrict__ x, ValT *__restrict__ y, int64_t items, int64_t J,    \
+        const int64_t *__restrict__ bound_tile, int64_t *__restrict__ carry_tile,                     \
+        double *__restrict__ carry_val, Probe probe, PeerOut po, const ValT *__restrict__ xh
+template <class OffT, class ValT, bool PROBE, bool VEC, bool PEERS = false, bool HOT = false>
+__global__ void __launch_bounds__(WoCfg<ValT>::NT) k_wo_chunk(LW_WO_PARAMS) {
+    wo_chunk_body<OffT, ValT, PROBE, VEC, PEERS, HOT>(A, x, y, items, J, bound_tile, carry_tile, carry_val,
+                                                      probe, po, xh);
+}
+template <class OffT, class ValT, bool PROBE, bool VEC, bool PEERS = false, bool HOT = false>
+__global__ void __launch_bounds__(WoCfg<ValT>::NT) __maxnreg__(PROBE ? 128 : WoCfg<double>::MAXR + (PEERS ? 8 : 0))
+    k_wo_chunk64(LW_WO_PARAMS) {
+    wo_chunk_body<OffT, ValT, PROBE, VEC, PEERS, HOT>(A, x, y, items, J, bound_tile, carry_tile, carry_val,
+                                                      probe, po, xh);
+}
+#undef LW_WO_PARAMS
+template <class OffT, class ValT, bool PROBE, bool VEC, bool PEERS = false, bool HOT = false>
+constexpr auto wo_chunk_kernel() {
+    if constexpr (sizeof(ValT) == 8) return &k_wo_chunk64<OffT, ValT, PROBE, VEC, PEERS, HOT>;
+    else return &k_wo_chunk<OffT, ValT, PROBE, VEC, PEERS, HOT>;
 }
 
 // ---- 3. ordered carry fix-up -----------------------------------------------------
@@ -742,7 +783,7 @@ template <class OffT, class ValT, bool PR, bool VEC, bool HOT = false>
 static int launch_chunk(const Csr<OffT, ValT>& a, const ValT* x, ValT* y, const WoPlan& p,
                         const int64_t* tiles, int64_t* c_tile, double* c_val, const Probe& pr,
                         cudaStream_t s, const ValT* xh = nullptr) {
-    auto kern = k_wo_chunk<OffT, ValT, PR, VEC, false, HOT>;
+    auto kern = wo_chunk_kernel<OffT, ValT, PR, VEC, false, HOT>();
     constexpr size_t smem = WoSmem<ValT>::bytes;
     static bool attr = false;   // one-time opt-in above the 48 KB default
     if (!attr) {
@@ -829,8 +870,8 @@ static int launch_wo_peers(const lw_csr_t* A, const void* x, void* y, const WoPl
     if (rc) return rc;
     const bool vec = ((uintptr_t)A->col_indices % 32 == 0) && ((uintptr_t)A->values % 32 == 0);
     constexpr size_t smem = WoSmem<ValT>::bytes;
-    auto kern = vec ? k_wo_chunk<OffT, ValT, false, true, true, HOT>
-                    : k_wo_chunk<OffT, ValT, false, false, true, HOT>;
+    auto kern = vec ? wo_chunk_kernel<OffT, ValT, false, true, true, HOT>()
+                    : wo_chunk_kernel<OffT, ValT, false, false, true, HOT>();
     ValT* xh = nullptr;
     if constexpr (HOT) {   // packed hot x after the base workspace, as in launch_wo
         xh = (ValT*)W.end;
