@@ -85,26 +85,71 @@ __global__ void k_scale(const ValT* y, int64_t n, const double* __restrict__ nor
     }
 }
 
-// The same per-element formula on 16-byte vectors (4 fp32 / 2 fp64 per load):
-// independent divisions per thread keep the loads in flight (the scalar loop
-// serialises load -> fp64 divide -> store). Results are identical.
+// x = y / ||y|| per element, rounded like (ValT)((double)y / nrm).
+// fp32: the fp64 quotient by Markstein's correction of a reciprocal multiply —
+// inv = RN(1/b) (one IEEE division per thread), q0 = RN(a*inv), r = a - b*q0
+// (exact by FMA), q = RN(q0 + r*inv) — which is RN(a/b) whenever inv is the
+// correctly rounded reciprocal and no intermediate leaves the normal range
+// (Markstein 1990; the IEEE fp64 divide does the same plus a slow path for
+// range extremes). Here a is an fp32 value widened to fp64 (|a| < 2^128) and b a
+// norm of fp32 values (2^-149 <= b < 2^141), so q0, r and r*inv stay far inside
+// fp64's normal range: the result is bit-identical to the division
+// (tests/test_gpu_parity.py checks it over every fp32 exponent). Non-finite a
+// gives a NaN residual and a = +-0 a +0 correction; q0 (= a / b for inf, NaN
+// and signed zeros) is returned then.
+// fp64 keeps the IEEE division (a may be tiny enough for r to underflow).
 template <class ValT>
-__global__ void k_scale_vec(const ValT* y, int64_t n, const double* __restrict__ norm,
-                            ValT* x) {   // x may be y
-    constexpr int V = 16 / sizeof(ValT);
+__device__ __forceinline__ ValT div_norm(ValT v, double b, double inv) {
+    if constexpr (sizeof(ValT) == 4) {
+        const double a = (double)v;
+        const double q0 = a * inv;
+        const double q = fma(fma(-q0, b, a), inv, q0);
+        return (ValT)(q == q && q0 != 0.0 ? q : q0);
+    } else {
+        return (ValT)((double)v / b);
+    }
+}
+
+// 16-byte vectors (4 fp32 / 2 fp64), U of them per thread in flight before the
+// first divide (one vector per thread left the loop latency-bound: 215 us for
+// 2^26 fp32 in the C5 loop, 2.4 TB/s).
+template <class ValT>
+__global__ void __launch_bounds__(256) k_scale_vec(const ValT* y, int64_t n, const double* __restrict__ norm,
+                                                   ValT* x) {   // x may be y
+    constexpr int V = 16 / sizeof(ValT), U = 4;
     using Vec = typename std::conditional<sizeof(ValT) == 4, float4, double2>::type;
-    const double nrm = norm[0];
+    const double b = norm[0];
+    if (!(b > 0.0)) {   // y = 0: x = y
+        if (x == y) return;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+            x[i] = y[i];
+        return;
+    }
+    const double inv = 1.0 / b;
     const int64_t nv = n / V;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + (U - 1) * stride < nv; i += U * stride) {
+        Vec v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = reinterpret_cast<const Vec*>(y)[i + u * stride];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            ValT* e = reinterpret_cast<ValT*>(&v[u]);
+#pragma unroll
+            for (int k = 0; k < V; ++k) e[k] = div_norm(e[k], b, inv);
+            reinterpret_cast<Vec*>(x)[i + u * stride] = v[u];
+        }
+    }
+    for (; i < nv; i += stride) {
         Vec v = reinterpret_cast<const Vec*>(y)[i];
         ValT* e = reinterpret_cast<ValT*>(&v);
 #pragma unroll
-        for (int k = 0; k < V; ++k) e[k] = nrm > 0.0 ? (ValT)((double)e[k] / nrm) : e[k];
+        for (int k = 0; k < V; ++k) e[k] = div_norm(e[k], b, inv);
         reinterpret_cast<Vec*>(x)[i] = v;
     }
     const int64_t t = nv * V + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // tail
-    if (t < n) x[t] = nrm > 0.0 ? (ValT)((double)y[t] / nrm) : y[t];
+    if (t < n) x[t] = div_norm(y[t], b, inv);
 }
 
 size_t norm_workspace(int64_t n) { return (size_t)(n > 0 ? ceil_div(n, VO_ITEMS) : 1) * 8; }
@@ -129,7 +174,7 @@ int vector_scale(const void* y, int64_t n, int dtype, const double* norm, void* 
     if (vec) {
         const int64_t nv = n / (dtype == LW_F32 ? 4 : 2);
         const unsigned gv = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nv, 256),
-                                                                          (int64_t)sm_count() * 16));
+                                                                          (int64_t)sm_count() * 8));
         if (dtype == LW_F32) k_scale_vec<float><<<gv, 256, 0, s>>>((const float*)y, n, norm, (float*)x);
         else k_scale_vec<double><<<gv, 256, 0, s>>>((const double*)y, n, norm, (double*)x);
     } else if (dtype == LW_F32) {

@@ -453,6 +453,41 @@ def test_device_normalisation(dtype):
     assert float(nz) == 0.0 and torch.equal(xz, z)
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_vector_scale_bit_exact_division(dtype):
+    """lw_vector_scale equals (ValT)((double)y / nrm) bit for bit — for fp32 via the
+    corrected reciprocal multiply (vector_ops.cu div_norm) — over random bit
+    patterns covering every fp32 exponent (denormals, +-0, inf, NaN included),
+    for norms from 2^-149 to 2^141, in place and out of place, odd lengths."""
+    from paper_2301_04792_b200 import _lib
+    from paper_2301_04792_b200.device import _dtype_code, current_stream
+
+    lib = _lib.load()
+    g = torch.Generator(device="cuda").manual_seed(11)
+    n = (1 << 22) + 3
+    if dtype == torch.float32:
+        bits = torch.randint(-(1 << 31), 1 << 31, (n,), generator=g, device="cuda", dtype=torch.int64)
+        y = bits.to(torch.int32).view(torch.float32)
+        y[:4] = torch.tensor([0.0, -0.0, float("inf"), float("nan")], device="cuda")
+    else:
+        y = torch.randn(n, generator=g, device="cuda", dtype=dtype) * 1e3
+    stream = current_stream(y.device)
+    for b in (2.0 ** -149, 1e-30, 0.0071, 1.0 / 3.0, 1.0, 3.0, 1234.5678, 7.3e5, 1e30, 2.0 ** 141,
+              float(torch.rand(1, generator=g, device="cuda")) * 1e4):
+        nrm = torch.tensor(b, dtype=torch.float64, device="cuda")
+        want = (y.double() / nrm).to(dtype)
+        out = torch.empty_like(y)
+        _lib.check(lib.lw_vector_scale(y.data_ptr(), n, _dtype_code(dtype), nrm.data_ptr(), out.data_ptr(),
+                                       stream), "lw_vector_scale")
+        yy = y.clone()
+        _lib.check(lib.lw_vector_scale(yy.data_ptr(), n, _dtype_code(dtype), nrm.data_ptr(), yy.data_ptr(),
+                                       stream), "lw_vector_scale")
+        for got in (out, yy):
+            iview = torch.int32 if dtype == torch.float32 else torch.int64
+            same = (got.view(iview) == want.view(iview)) | (torch.isnan(got) & torch.isnan(want))
+            assert bool(same.all()), f"norm {b}: {int((~same).sum())} elements differ"
+
+
 def test_power_iteration_graph_replay_matches_eager():
     """The CUDA-graph-captured power iteration replays the exact eager iterates."""
     from paper_2301_04792_b200.distributed import (RowShard, nnz_balanced_bounds, power_iteration,

@@ -44,11 +44,16 @@ def run(nt, ntma, c, tag, reps=10):
     o = out.clone()
     if ntma == 0:
         ref[key] = o
-    same = bool(torch.allclose(o, ref[key], rtol=1e-5, atol=1e-5)) if key in ref else None
+    same = bool(torch.allclose(o, ref[key], rtol=1e-5, atol=1e-5)) if key in ref and ntma >= 0 else None
     print(json.dumps({"cols": tag, "nt": nt, "ntma": ntma, "ms": round(ms, 4),
                       "Ggather_s": round(n / ms / 1e6, 1), "same_as_lsu": same}), flush=True)
 
 
+if len(sys.argv) > 1 and sys.argv[1] == "tr":
+    for tag, c in (("c3", col), ("uniform", ucol)):
+        run(512, 0, c, tag)
+        run(512, -1, c, tag)
+    sys.exit(0)
 for tag, c in (("c3", col), ("uniform", ucol)):
     for nt in (512, 256):
         for ntma in (0, 4, 8):

@@ -79,6 +79,30 @@ __global__ void __launch_bounds__(NT) k_tg(const __grid_constant__ CUtensorMap t
     out[seg * NT + tid] = acc;
 }
 
+// ntma = -1: "transposed" atom order — gather instruction k of a warp reads the
+// 32 consecutive atoms 32k + lane of the warp's 256-atom block (sorted columns of
+// one row sit side by side in one instruction), instead of atom 8*lane + k.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_tr(const int* __restrict__ col, const float* __restrict__ val,
+                                           const float* __restrict__ x, float* __restrict__ out, long nseg) {
+    const long seg = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long b = (seg * NT + warp * 32) * 8;
+    int c[8];
+    float v[8], g[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(c[k]) : "l"(col + b + 32 * k + lane));
+        asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v[k]) : "l"(val + b + 32 * k + lane));
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(g[k]) : "l"(x + c[k]));
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc += v[k] * g[k];
+    out[seg * NT + threadIdx.x] = acc;
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 encode() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
@@ -117,6 +141,10 @@ extern "C" int tma_gather(int nt, int ntma, const int* col, const float* val, co
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return 1000 + (int)r;
     const long nseg = n / (8L * nt);
+    if (ntma == -1 && nt == 512) {
+        k_tr<512><<<(unsigned)nseg, 512, 0, s>>>(col, val, x, out, nseg);
+        return (int)cudaGetLastError();
+    }
 #define LW_TG(NT_, K_) \
     if (nt == NT_ && ntma == K_) return launch<NT_, K_>(tm, col, val, x, out, nseg, s);
     LW_TG(512, 0) LW_TG(512, 4) LW_TG(512, 8) LW_TG(256, 0) LW_TG(256, 4) LW_TG(256, 8) LW_TG(128, 4)
