@@ -241,8 +241,9 @@ int lw_spmv_host(int schedule, const lw_csr_t* A_host, const void* x_host, void*
  * team of threads covering up to 32x16 bytes of columns; wider n is walked in
  * slabs. B and C are device pointers; 16-byte aligned B/C with n a multiple of
  * 4 (fp32) / 2 (fp64) take the vector path. lanes = 0 selects
- * lw_spmm_auto_lanes(). Sums are fp64; group_mapped zeroes C and accumulates
- * with atomics (like the reference's C += v * B[src]). */
+ * lw_spmm_auto_lanes(). Sums are fp64; group_mapped sums each C[tile, :] in the
+ * reference's member-major C += v * B[src] order (no atomics; bit-identical to
+ * the reference for fp64 data). */
 int lw_spmm_auto_lanes(int schedule, int64_t rows, int64_t nnz, int64_t n, int64_t group_size,
                        int64_t tiles_per_block, int64_t* lanes_out);
 size_t lw_spmm_workspace(int schedule, int64_t rows, int64_t nnz, int64_t n, int64_t lanes,

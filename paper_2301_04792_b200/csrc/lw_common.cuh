@@ -57,9 +57,15 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+#ifndef LW_X_POLICY   // A/B: L2 policy of the x gathers (0 evict_last, 1 evict_normal, 2 evict_first, 3 evict_last on 40%)
+#define LW_X_POLICY 0
+#endif
 __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t p;
-    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    if (LW_X_POLICY == 1) asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    else if (LW_X_POLICY == 2) asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    else if (LW_X_POLICY == 3) asm("createpolicy.fractional.L2::evict_last.L2::evict_unchanged.b64 %0, 0.4;" : "=l"(p));
+    else asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
 __device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
@@ -133,6 +139,38 @@ __device__ __forceinline__ R warp_segsum_heads(R v, int lane, uint32_t heads) {
     }
     return v;
 }
+
+// Positions [e0, e1) of one tile of a group_mapped block in the reference's
+// member-major order (_fast.py:66-77): member m of M takes block-local positions
+// k = m (mod M), so position e0 + i belongs to member (r0 + i) mod M with
+// r0 = e0 mod M. Members in ascending order are the offsets
+// i = M - r0, ..., rs - 1 (wrapped residues 0, 1, ...), then i = 0, ..., M - r0 - 1
+// (residues r0, ..., M - 1), rs = min(e1 - e0, M); each member's positions step
+// by M. next() yields them one by one (-1 when done).
+struct MemberMajorWalk {
+    int64_t e0, e1, M, split, rs, i, k;
+    __host__ __device__ MemberMajorWalk(int64_t e0_, int64_t e1_, int64_t M_) : e0(e0_), e1(e1_), M(M_) {
+        const int64_t n = e1 - e0;
+        rs = n < M ? n : M;
+        split = n > 0 ? M - e0 % M : 0;     // offsets >= split are the wrapped residues
+        i = split < rs ? split : 0;
+        k = n > 0 ? e0 + i : e1;
+    }
+    __host__ __device__ __forceinline__ int64_t next() {
+        if (k >= e1) return -1;
+        const int64_t r = k;
+        k += M;
+        if (k >= e1) {   // this member is done: the next member's first position
+            if (i >= split) {                                   // wrapped residues, then offset 0
+                i = i + 1 < rs ? i + 1 : 0;                     // (offset 0 exists: split >= 1)
+                k = e0 + i;
+            } else if (i + 1 < (rs < split ? rs : split)) {
+                k = e0 + ++i;
+            }                                                   // else k stays >= e1: done
+        }
+        return r;
+    }
+};
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

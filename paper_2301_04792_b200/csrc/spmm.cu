@@ -259,60 +259,92 @@ __global__ void k_spmm_carry_fixup(const int64_t* __restrict__ carry_tile,
 }
 
 // ---- group_mapped: groups own blocks of tiles, members stride atoms (_fast.py:121-144) --
-// Lane = (group g, member m); C is zeroed first and accumulated, like the
-// reference (kernels.py:164-175 writes C += v * B[src]).
-template <class ValT>
-__device__ __forceinline__ void atomic_add_out(ValT* p, double v) {
-    atomicAdd(p, (ValT)v);
-}
-
+// The reference adds v * B[src, c] into C[tile, c] member by member: member 0's
+// atoms of the tile in increasing order, then member 1's, ... (member m of the
+// group owning the tile's block takes block-local atoms m, m + M, ...). One team
+// per tile replays that order per column with unfused fp64 multiply and add
+// (the SpMV k_group_tiles walk): C is written once per tile, run-to-run
+// identical and, for fp64 data, bit-identical to the reference — no atomics,
+// no zeroing pass.
+constexpr int GT_U = 4;   // atoms per residue batch (loads in flight)
 template <class OffT, class ValT, int VEC>
 __global__ void __launch_bounds__(MM_NT)
-    k_spmm_group_mapped(Csr<OffT, ValT> A, const ValT* __restrict__ B, ValT* __restrict__ C,
-                        int64_t n, int64_t lanes, int64_t gs, int64_t tpb, int lg_ts) {
+    k_spmm_group_tiles(Csr<OffT, ValT> A, const ValT* __restrict__ B, ValT* __restrict__ C, int64_t n,
+                       int64_t lanes, int64_t gs, int64_t tpb, int lg_ts) {
     const int64_t gt = (int64_t)blockIdx.x * MM_NT + threadIdx.x;
-    const int64_t lane = gt >> lg_ts;
+    const int64_t t = gt >> lg_ts;
     const int tl = (int)(gt & ((1 << lg_ts) - 1));
-    if (lane >= lanes) return;
+    if (t >= A.rows) return;
     const int64_t groups = (lanes + gs - 1) / gs;
-    const int64_t g = lane / gs, m = lane - g * gs;
-    const int64_t members = min(gs, lanes - g * gs);
-    const int64_t blocks = (A.rows + tpb - 1) / tpb;
-    const int64_t sw = ((int64_t)VEC) << lg_ts;
-    // Slabs outermost: a member's consecutive atoms usually stay in one tile, so its
-    // products are summed in registers and added to C once per tile run (the
-    // atomics of the reference's C[tile] += v*B[src] are per run, not per atom).
+    const int64_t b = t / tpb, g = b % groups;
+    const int64_t M = min(gs, lanes - g * gs);
+    const int64_t base = (int64_t)__ldg(A.off + b * tpb);
+    const int64_t e0 = (int64_t)__ldg(A.off + t) - base, e1 = (int64_t)__ldg(A.off + t + 1) - base;
+    const int64_t sw = ((int64_t)VEC) << lg_ts;   // slab width
     for (int64_t cs = 0; cs < n; cs += sw) {
         const int64_t c = cs + (int64_t)tl * VEC;
         if (c >= n) continue;
-        for (int64_t b = g; b < blocks; b += groups) {
-            const int64_t tb = b * tpb, tc = min(tpb, A.rows - tb);
-            const int64_t base = (int64_t)__ldg(A.off + tb), tot = (int64_t)__ldg(A.off + tb + tc) - base;
-            int64_t t = tb, cur = -1;
-            double acc[VEC];
+        double acc[VEC];
 #pragma unroll
-            for (int j = 0; j < VEC; ++j) acc[j] = 0.0;
-            for (int64_t k = m; k < tot; k += members) {
-                const int64_t a = base + k;
-                while ((int64_t)__ldg(A.off + t + 1) <= a) ++t;   // get_tile by monotone advance
-                if (t != cur) {
-                    if (cur >= 0)
+        for (int j = 0; j < VEC; ++j) acc[j] = 0.0;
+        if (e1 - e0 >= GT_U * M) {
+            // long tile: member by member (same order), GT_U of a member's atoms
+            // (stride M) in flight per batch — no walker arithmetic per atom
+            const int64_t r0 = e0 % M;
+            auto member = [&](int64_t i) {
+                for (int64_t k0 = e0 + i; k0 < e1; k0 += GT_U * M) {
+                    int32_t col[GT_U];
+                    double v[GT_U];
 #pragma unroll
-                        for (int j = 0; j < VEC; ++j) atomic_add_out(C + cur * n + c + j, acc[j]);
-                    cur = t;
+                    for (int u = 0; u < GT_U; ++u) {
+                        const int64_t k = k0 + u * M < e1 ? k0 + u * M : k0;
+                        col[u] = __ldg(A.col + base + k);
+                        v[u] = (double)__ldg(A.val + base + k);
+                    }
+                    ValT bv[GT_U][VEC];
 #pragma unroll
-                    for (int j = 0; j < VEC; ++j) acc[j] = 0.0;
+                    for (int u = 0; u < GT_U; ++u) ld_row<ValT, VEC>(B + (int64_t)col[u] * n + c, bv[u]);
+#pragma unroll
+                    for (int u = 0; u < GT_U; ++u)
+                        if (k0 + u * M < e1)
+#pragma unroll
+                            for (int j = 0; j < VEC; ++j) acc[j] = __dadd_rn(acc[j], __dmul_rn(v[u], (double)bv[u][j]));
                 }
-                const double v = (double)__ldg(A.val + a);
-                ValT bv[VEC];
-                ld_row<ValT, VEC>(B + (int64_t)__ldg(A.col + a) * n + c, bv);
-#pragma unroll
-                for (int j = 0; j < VEC; ++j) acc[j] = fma(v, (double)bv[j], acc[j]);
-            }
-            if (cur >= 0)
-#pragma unroll
-                for (int j = 0; j < VEC; ++j) atomic_add_out(C + cur * n + c + j, acc[j]);
+            };
+            for (int64_t i = M - r0; i < M; ++i) member(i);   // wrapped residues 0, 1, ... first
+            for (int64_t i = 0; i < M - r0; ++i) member(i);
+            st_row<ValT, VEC>(C + t * n + c, acc);
+            continue;
         }
+        MemberMajorWalk w(e0, e1, M);
+        for (int64_t p0 = w.next(); p0 >= 0;) {   // GT_U atoms' loads in flight, then the ordered adds
+            int64_t k[GT_U];
+            k[0] = p0;
+#pragma unroll
+            for (int u = 1; u < GT_U; ++u) k[u] = k[u - 1] >= 0 ? w.next() : -1;
+            int32_t col[GT_U];
+            double v[GT_U];
+#pragma unroll
+            for (int u = 0; u < GT_U; ++u) {
+                col[u] = k[u] >= 0 ? __ldg(A.col + base + k[u]) : 0;
+                v[u] = k[u] >= 0 ? (double)__ldg(A.val + base + k[u]) : 0.0;
+            }
+            ValT bv[GT_U][VEC];
+#pragma unroll
+            for (int u = 0; u < GT_U; ++u) {
+                if (k[u] >= 0) ld_row<ValT, VEC>(B + (int64_t)col[u] * n + c, bv[u]);
+                else
+#pragma unroll
+                    for (int j = 0; j < VEC; ++j) bv[u][j] = (ValT)0;
+            }
+#pragma unroll
+            for (int u = 0; u < GT_U; ++u)
+                if (k[u] >= 0)
+#pragma unroll
+                    for (int j = 0; j < VEC; ++j) acc[j] = __dadd_rn(acc[j], __dmul_rn(v[u], (double)bv[u][j]));
+            p0 = k[GT_U - 1] >= 0 ? w.next() : -1;
+        }
+        st_row<ValT, VEC>(C + t * n + c, acc);
     }
 }
 
@@ -407,11 +439,13 @@ static int spmm_typed(int schedule, const lw_csr_t* H, const void* Bp, void* Cp,
             LW_LAUNCH_CHECK();
             return LW_OK;
         }
-        case LW_GROUP_MAPPED:
-            LW_TRY(cudaMemsetAsync(C, 0, (size_t)A.rows * (size_t)n * sizeof(ValT), s));
-            LW_MM_DISPATCH(k_spmm_group_mapped, A, B, C, n, lanes, gs, tpb, sh.lg_ts);
+        case LW_GROUP_MAPPED: {
+            const unsigned tgrid = mm_grid(A.rows, sh.lg_ts);   // one team per tile
+            if (sh.vec == V) k_spmm_group_tiles<OffT, ValT, V><<<tgrid, MM_NT, 0, s>>>(A, B, C, n, lanes, gs, tpb, sh.lg_ts);
+            else k_spmm_group_tiles<OffT, ValT, 1><<<tgrid, MM_NT, 0, s>>>(A, B, C, n, lanes, gs, tpb, sh.lg_ts);
             LW_LAUNCH_CHECK();
             return LW_OK;
+        }
         default: return LW_E_INVALID_ARG;
     }
 #undef LW_MM_DISPATCH

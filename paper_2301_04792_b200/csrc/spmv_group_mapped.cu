@@ -21,10 +21,12 @@
 //    CTA is a group; the plan is a block-wide scan into shared memory, atom ->
 //    tile is a log2(NT)-probe search in shared memory, per-warp shared
 //    accumulators (combined in warp order) keep the result deterministic.
-//  * k_group_generic (any group_size / tiles_per_block / lane count): one thread
-//    per lane running the reference's member loop over global memory, with a
-//    monotone tile advance (_fast.py:75-76) and atomic adds into a zeroed y (the
-//    reference's pre-zeroed y += v*x, kernels.py:63 / _fast.py:77).
+//  * any other group_size / tiles_per_block / lane count: k_group_tiles, one
+//    thread per tile summing the tile's atoms in the reference's member-major
+//    order (bit-identical to the reference's fp64 y, deterministic); probe runs
+//    first execute k_group_generic — one thread per lane running the reference's
+//    member loop with a monotone tile advance (_fast.py:75-76) — to record the
+//    lane -> atom -> tile assignment.
 #include <algorithm>
 #include <climits>
 #include <type_traits>
@@ -511,6 +513,76 @@ __global__ void __launch_bounds__(256)
     if (PROBE && probe.lane_atoms) probe.lane_atoms[l] = mine;
 }
 
+// ---- general groups: y in the reference's member-major order ---------------------------
+// The reference accumulates y[tile] += v*x member by member (_fast.py:66-77): member
+// 0's atoms of the tile in increasing order, then member 1's, ... in fp64. One
+// thread per tile replays exactly that order (MemberMajorWalk, lw_common.cuh) with
+// unfused fp64 multiply and add, GT_U positions' loads in flight at a time. y is therefore run-to-run identical and, for fp64 data,
+// bit-identical to the reference's spmv (tests: golden group configs compared
+// exactly); no atomics, no zeroing pass. The lane -> atom mapping of these shapes
+// is what k_group_generic executes (probe runs, which then rewrite y with this).
+constexpr int GT_U = 8;   // positions per residue batch (loads in flight)
+template <class OffT, class ValT>
+__global__ void __launch_bounds__(256)
+    k_group_tiles(Csr<OffT, ValT> A, const ValT* __restrict__ x, ValT* __restrict__ y, int64_t lanes,
+                  int64_t gs, int64_t tpb) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= A.rows) return;
+    const int64_t groups = (lanes + gs - 1) / gs;
+    const int64_t b = t / tpb, g = b % groups;
+    const int64_t M = min(gs, lanes - g * gs);   // members of the group owning block b
+    const int64_t base = ld_off(A.off + b * tpb);
+    const int64_t e0 = ld_off(A.off + t) - base, e1 = ld_off(A.off + t + 1) - base;
+    double acc = 0.0;
+    if (e1 - e0 >= GT_U * M) {
+        // long tile: member by member (same order), GT_U of a member's positions
+        // (stride M) in flight per batch, no walker arithmetic per position
+        const int64_t r0 = e0 % M;
+        auto member = [&](int64_t i) {
+            for (int64_t k0 = e0 + i; k0 < e1; k0 += GT_U * M) {
+                int32_t c[GT_U];
+                double v[GT_U], xv[GT_U];
+#pragma unroll
+                for (int u = 0; u < GT_U; ++u) {
+                    const int64_t k = k0 + u * M < e1 ? k0 + u * M : k0;
+                    c[u] = __ldg(A.col + base + k);
+                    v[u] = (double)__ldg(A.val + base + k);
+                }
+#pragma unroll
+                for (int u = 0; u < GT_U; ++u) xv[u] = (double)ld_gather(x + c[u]);
+#pragma unroll
+                for (int u = 0; u < GT_U; ++u)
+                    if (k0 + u * M < e1) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
+            }
+        };
+        for (int64_t i = M - r0; i < M; ++i) member(i);   // wrapped residues 0, 1, ... first
+        for (int64_t i = 0; i < M - r0; ++i) member(i);
+        y[t] = (ValT)acc;
+        return;
+    }
+    MemberMajorWalk w(e0, e1, M);
+    for (int64_t p0 = w.next(); p0 >= 0;) {   // GT_U positions' loads in flight, then the ordered adds
+        int64_t k[GT_U];
+        k[0] = p0;
+#pragma unroll
+        for (int u = 1; u < GT_U; ++u) k[u] = k[u - 1] >= 0 ? w.next() : -1;
+        int32_t c[GT_U];
+        double v[GT_U], xv[GT_U];
+#pragma unroll
+        for (int u = 0; u < GT_U; ++u) {
+            c[u] = k[u] >= 0 ? __ldg(A.col + base + k[u]) : 0;
+            v[u] = k[u] >= 0 ? (double)__ldg(A.val + base + k[u]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < GT_U; ++u) xv[u] = k[u] >= 0 ? (double)ld_gather(x + c[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < GT_U; ++u)
+            if (k[u] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
+        p0 = k[GT_U - 1] >= 0 ? w.next() : -1;
+    }
+    y[t] = (ValT)acc;
+}
+
 // ---- host side ----------------------------------------------------------------------
 enum GroupKernel { GK_WARP, GK_BLOCK, GK_GENERIC };
 
@@ -605,10 +677,12 @@ static int launch_group(const lw_csr_t* A, const void* x, void* y, int64_t lanes
             break;
         }
         default: {
-            LW_TRY(cudaMemsetAsync(y, 0, A->rows * sizeof(ValT), s));
-            const int64_t grid = ceil_div(lanes, 256);
-            if (probe) k_group_generic<OffT, ValT, true><<<grid, 256, 0, s>>>(a, xv, yv, lanes, gs, tpb, p);
-            else       k_group_generic<OffT, ValT, false><<<grid, 256, 0, s>>>(a, xv, yv, lanes, gs, tpb, p);
+            if (probe) {   // the lane -> atom instrumentation, then y in the reference order
+                LW_TRY(cudaMemsetAsync(y, 0, A->rows * sizeof(ValT), s));
+                k_group_generic<OffT, ValT, true><<<ceil_div(lanes, 256), 256, 0, s>>>(a, xv, yv, lanes, gs, tpb, p);
+                LW_LAUNCH_CHECK();
+            }
+            k_group_tiles<OffT, ValT><<<ceil_div(A->rows, 256), 256, 0, s>>>(a, xv, yv, lanes, gs, tpb);
         }
     }
     LW_LAUNCH_CHECK();
