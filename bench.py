@@ -61,7 +61,7 @@ def parse():
     ap.add_argument("--dtype", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--hot-x", default="auto", choices=["auto", "on", "off"],
-                    help="work_oriented: hot-x column packing (DESIGN.md 4e); auto = fp32 only")
+                    help="work_oriented: hot-x column packing (DESIGN.md 4e); auto = on (fp32 and fp64)")
     ap.add_argument("--max-hot", type=int, default=0, help="hot-x slots (0 = library default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -357,7 +357,7 @@ def power_measure(args, world, rank, local, dev, scale, seed):
     y_local = torch.empty(A.rows, dtype=A.dtype, device=dev)
     chunks = args.chunks or (4 if world > 1 else 1)
     # hot-x packing of every SpMV operand (one-time, before warm-up)
-    hot = args.hot_x == "on" or (args.hot_x == "auto" and args.dtype == "fp32")
+    hot = args.hot_x in ("on", "auto")
     spmv_ev = []
     layout = None
     if not (args.fused or args.graph):
@@ -524,8 +524,7 @@ def our_arm(args):
     # hot-x column packing (one-time inspector, outside the timed region like the
     # matrix upload): fp32 work_oriented by default, measured slower for fp64
     hx, hx_build_ms = None, None
-    if sched is lwb.ScheduleKind.MERGE_PATH and (args.hot_x == "on" or
-                                                 (args.hot_x == "auto" and args.dtype == "fp32")):
+    if sched is lwb.ScheduleKind.MERGE_PATH and args.hot_x in ("on", "auto"):
         torch.cuda.synchronize()
         t_b = time.perf_counter()
         hx = A.pack_hot_columns(args.max_hot or None)
@@ -706,7 +705,8 @@ def our_arm(args):
 
 def fp64_leg(A, args, lib, dev, world, nnz_total, hbm):
     """The same C3 matrix with fp64 values (the reference's only precision,
-    sparse.py:55-58): work_oriented kernel, unpacked, timed like the headline."""
+    sparse.py:55-58): work_oriented kernel, hot-x packed like the headline (and
+    unpacked beside it, y compared bit for bit), timed like the headline."""
     import torch
     import torch.distributed as dist
 
@@ -716,29 +716,45 @@ def fp64_leg(A, args, lib, dev, world, nnz_total, hbm):
     x = torch.ones(A64.cols, dtype=torch.float64, device=dev)
     y = torch.empty(A64.rows, dtype=torch.float64, device=dev)
     cfg = lwb.ExecutorConfig(schedule=lwb.ScheduleKind.MERGE_PATH)
-    for _ in range(max(args.warmup, 3)):
-        lwb.spmv(A64, x, cfg, out=y)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(args.steps):
-        lwb.spmv(A64, x, cfg, out=y)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t[0])
+
+    def timed():
+        for _ in range(max(args.warmup, 3)):
+            lwb.spmv(A64, x, cfg, out=y)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            lwb.spmv(A64, x, cfg, out=y)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t[0])
+        return ms
+
+    ms_plain = timed()
+    y_plain = y.clone()
+    packed = args.hot_x in ("on", "auto")
+    ms = ms_plain
+    if packed:
+        A64.pack_hot_columns(args.max_hot or None)
+        ms = timed()
     alg = A64.algorithmic_bytes()
     out = {"dtype": "f64", "ms_per_step": round(ms, 4),
            "value": round(2.0 * nnz_total / (ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
            "hbm_gbs_step": round(alg / (ms * 1e-3) / 1e9, 1),
            "frac_step": round(alg / (ms * 1e-3) / 1e9 / hbm, 4), "alg_bytes": alg,
-           "path": "lw_spmv_work_oriented (fp64 values and x, int32 columns), 3 launches per step"}
-    del A64, x, y
+           "path": ("lw_spmv_work_oriented_hotx" if packed else "lw_spmv_work_oriented")
+                   + " (fp64 values and x, int32 columns), 3 launches per step"}
+    if packed:
+        out["unpacked"] = {"ms_per_step": round(ms_plain, 4),
+                           "value": round(2.0 * nnz_total / (ms_plain * 1e-3) / 1e9, 3),
+                           "y_bit_identical": bool(torch.equal(y, y_plain))}
+    del A64, x, y, y_plain
     torch.cuda.empty_cache()
     return out
 
