@@ -55,9 +55,12 @@ template <>
 struct WoCfg<float> {
     static constexpr int NT = LW_WO_NT, IPT = WO_W / LW_WO_NT, MAXR = 0;   // uncapped
 };
+#ifndef LW_WO_MAXR64
+#define LW_WO_MAXR64 40
+#endif
 template <>
 struct WoCfg<double> {
-    static constexpr int NT = LW_WO_NT, IPT = WO_W / LW_WO_NT, MAXR = 40;
+    static constexpr int NT = LW_WO_NT, IPT = WO_W / LW_WO_NT, MAXR = LW_WO_MAXR64;
 };
 
 // ---- 1. partition ---------------------------------------------------------
