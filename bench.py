@@ -522,7 +522,7 @@ def our_arm(args):
         ws = torch.empty(max(ws_bytes, 256), dtype=torch.uint8, device=dev)
 
     # hot-x column packing (one-time inspector, outside the timed region like the
-    # matrix upload): fp32 work_oriented by default, measured slower for fp64
+    # matrix upload): work_oriented, both dtypes by default
     hx, hx_build_ms = None, None
     if sched is lwb.ScheduleKind.MERGE_PATH and args.hot_x in ("on", "auto"):
         torch.cuda.synchronize()
