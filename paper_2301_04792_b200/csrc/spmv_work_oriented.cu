@@ -34,6 +34,9 @@ namespace lw {
 #endif
 constexpr int WO_W = LW_WO_W;
 constexpr int WO_S = WO_W - 16;
+#ifndef LW_WO_PDL   // A/B: chunk and fix-up kernels as programmatic dependent launches
+#define LW_WO_PDL 1
+#endif
 #ifndef LW_WO_BATCH   // A/B: batch the unpacked kernel's gathers like the packed one's
 #define LW_WO_BATCH 0
 #endif
@@ -79,6 +82,7 @@ __global__ void k_merge_path_search(const OffT* __restrict__ off, int64_t rows, 
                                     int64_t* __restrict__ out_tile,
                                     int64_t* __restrict__ out_coords,
                                     unsigned* __restrict__ ticket = nullptr) {
+    if (LW_WO_PDL) pdl_trigger();   // the chunk kernel may launch; it waits for these results
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (ticket && k == 0) *ticket = 0u;   // the carry fix-up's CTA counter
     if (k >= n_bounds) return;
@@ -316,6 +320,7 @@ __device__ __forceinline__ void wo_chunk_body(Csr<OffT, ValT> A, const ValT* __r
         for (int p = 0; p < LW_MAX_PEERS; ++p) s_peer[p] = po.ptr[p];
     }
 
+    if (LW_WO_PDL) pdl_wait();   // chunk bounds and the packed hot x come from the partition launch
     const int tid = threadIdx.x, lane = tid & (kWarp - 1), warp = tid >> 5;
     const int64_t l = blockIdx.x;
     const int64_t total = A.rows + A.nnz;
@@ -541,6 +546,7 @@ __global__ void __launch_bounds__(FX_NT)
     __shared__ double s_sum[FX_NT / kWarp];
     __shared__ int s_has[FX_NT / kWarp];
     __shared__ bool s_last;
+    if (LW_WO_PDL) pdl_wait();   // carries come from the chunk kernel
     const int tid = threadIdx.x, lane = tid & (kWarp - 1), warp = tid >> 5;
     const int64_t c0 = (int64_t)blockIdx.x * FX_NT, c1 = min(c0 + FX_NT, n), i = c0 + tid;
     const bool in = i < c1;
@@ -654,6 +660,7 @@ __global__ void k_search_pack(const OffT* __restrict__ off, int64_t rows, int64_
                               int64_t* __restrict__ out_tile, unsigned nsb,
                               const ValT* __restrict__ x, const int32_t* __restrict__ hot_cols,
                               int32_t n_hot, ValT* __restrict__ xh, unsigned* __restrict__ ticket) {
+    if (LW_WO_PDL) pdl_trigger();   // the chunk kernel may launch; it waits for these results
     if (blockIdx.x == 0 && threadIdx.x == 0) *ticket = 0u;
     if (blockIdx.x >= nsb) {
         const int i = (int)(blockIdx.x - nsb) * blockDim.x + threadIdx.x;
@@ -735,8 +742,12 @@ template <class ValT, bool PEERS = false>
 static int launch_fixup(const WoWs& w, int64_t n, ValT* y, int64_t rows, cudaStream_t s,
                         const PeerOut& po = PeerOut{}) {
     if (n <= 0) return LW_OK;
-    k_carry_fixup<ValT, PEERS><<<(unsigned)ceil_div(n, (int64_t)FX_NT), FX_NT, 0, s>>>(
-        w.c_tile, w.c_val, n, y, rows, w.ticket, w.segs, po);
+    if (LW_WO_PDL)
+        LW_TRY(launch_pdl(k_carry_fixup<ValT, PEERS>, dim3((unsigned)ceil_div(n, (int64_t)FX_NT)), dim3(FX_NT), 0, s,
+                          w.c_tile, w.c_val, n, y, rows, w.ticket, w.segs, po));
+    else
+        k_carry_fixup<ValT, PEERS><<<(unsigned)ceil_div(n, (int64_t)FX_NT), FX_NT, 0, s>>>(
+            w.c_tile, w.c_val, n, y, rows, w.ticket, w.segs, po);
     LW_LAUNCH_CHECK();
     return LW_OK;
 }
@@ -795,8 +806,12 @@ static int launch_chunk(const Csr<OffT, ValT>& a, const ValT* x, ValT* y, const 
             LW_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv)));
         attr = true;
     }
-    kern<<<(unsigned)p.lanes, WoCfg<ValT>::NT, smem, s>>>(a, x, y, p.items, p.J, tiles, c_tile,
-                                                         c_val, pr, PeerOut{}, xh);
+    if (LW_WO_PDL)
+        LW_TRY(launch_pdl(kern, dim3((unsigned)p.lanes), dim3(WoCfg<ValT>::NT), smem, s, a, x, y, p.items, p.J,
+                          tiles, c_tile, c_val, pr, PeerOut{}, xh));
+    else
+        kern<<<(unsigned)p.lanes, WoCfg<ValT>::NT, smem, s>>>(a, x, y, p.items, p.J, tiles, c_tile,
+                                                             c_val, pr, PeerOut{}, xh);
     LW_LAUNCH_CHECK();
     return LW_OK;
 }
