@@ -26,7 +26,7 @@ def _dev(off, col, val, cols, dtype):
                      torch.as_tensor(col).cuda().to(torch.int32), torch.as_tensor(val).cuda().to(dtype))
 
 
-@pytest.mark.parametrize("lanes", [1500, 9000, 100_000])
+@pytest.mark.parametrize("lanes", [1500, 9000, 100_000, 1_500_000])
 def test_runs_crossing_fixup_ctas_integer_bit_exact(lanes):
     """Rows of 2..20000 atoms cut into many lanes: runs of carries of every
     length, many crossing the 1024-carry CTAs of the fix-up. Integer data: the
@@ -79,6 +79,17 @@ def test_one_row_spanning_every_lane(dtype):
     else:
         worst, row = oracle.worst_ratio(y, y_ref, scale, 1e-5)
         assert worst <= 1.0, (row, worst)
+
+
+def test_one_row_spanning_several_merge_passes():
+    """2.1 M lanes: the fix-up's last CTA merges > 4 K edge pieces in several
+    1024-slot passes, all of one run carried from pass to pass (integer data,
+    bit-exact)."""
+    m, x = _giant(torch.float64)
+    y = lwb.spmv(m, x, ExecutorConfig(schedule=WO, lanes=2_100_000)).cpu().numpy()
+    host = [t.cpu().numpy() for t in (m.row_offsets, m.col_indices, m.values)]
+    y_ref, _ = oracle.spmv_narrow(*host, x.cpu().numpy())
+    np.testing.assert_array_equal(y, y_ref)
 
 
 def test_fixup_cost_bounded_on_the_spanning_row():
