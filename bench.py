@@ -78,6 +78,8 @@ def parse():
                          "chunk's SpMV (0 = 4 when N > 1, else 1)")
     ap.add_argument("--items", type=int, default=0,
                     help="work_oriented items per lane (0 = library default)")
+    ap.add_argument("--balance", default="work", choices=["work", "nnz"],
+                    help="N > 1 row split: rows+nnz balanced (merge-path tiles, default) or nnz balanced")
     ap.add_argument("--relabel", default="on", choices=["on", "off"],
                     help="power mode: symmetric degree relabeling of the C5 operator (one-time)")
     ap.add_argument("--no-fp64", action="store_true", help="skip the fp64 C3 leg")
@@ -329,7 +331,7 @@ def power_measure(args, world, rank, local, dev, scale, seed):
     import torch.distributed as dist
 
     import paper_2301_04792_b200 as lwb
-    from paper_2301_04792_b200.distributed import RowShard, nnz_balanced_bounds, power_iteration
+    from paper_2301_04792_b200.distributed import RowShard, power_iteration, row_bounds
 
     dtype = "float32" if args.dtype == "fp32" else "float64"
     full = lwb.generate_rmat_csr(scale, args.edge_factor, seed, dtype=dtype, device=dev)
@@ -347,7 +349,7 @@ def power_measure(args, world, rank, local, dev, scale, seed):
         torch.cuda.synchronize()
         prep_ms["relabel"] = round((time.perf_counter() - t_r) * 1e3, 1)
         full = R.matrix
-    bounds = nnz_balanced_bounds(full.row_offsets.cpu().numpy(), world)
+    bounds = row_bounds(full.row_offsets.cpu().numpy(), world, args.balance)
     shard = RowShard(bounds, rank)
     A = full.row_slice(shard.r0, shard.r1)
     A = lwb.DeviceCsr(A.rows, A.cols, A.row_offsets.clone(), A.col_indices.clone(), A.values.clone())
@@ -448,6 +450,7 @@ def power_measure(args, world, rank, local, dev, scale, seed):
         "data": "synthetic",
         "config": {"workload": f"rmat{scale}-ef{args.edge_factor}-seed{seed}-power{args.iters}",
                    "rows": n, "nnz": nnz_total, "parallelism": f"rows{world}" if world > 1 else "single",
+                   "row_split": args.balance if world > 1 else None,
                    "overlap_chunks": 0 if (args.fused or args.graph) else chunks,
                    "fused_allgather": bool(args.fused), "cuda_graph": bool(args.graph),
                    "x_layout": ("degree-relabeled P A P^T (DESIGN.md 4f)" if relabel else "as generated")
@@ -475,7 +478,7 @@ def our_arm(args):
     import paper_2301_04792_b200 as lwb
     from paper_2301_04792_b200 import _lib
     from paper_2301_04792_b200.device import current_stream
-    from paper_2301_04792_b200.distributed import nnz_balanced_bounds
+    from paper_2301_04792_b200.distributed import row_bounds
 
     world, rank, local, dev = setup_ranks()
 
@@ -488,7 +491,7 @@ def our_arm(args):
     nnz_total = full.nnz
     rows_total = full.rows
     if world > 1:
-        bounds = nnz_balanced_bounds(full.row_offsets.cpu().numpy(), world)
+        bounds = row_bounds(full.row_offsets.cpu().numpy(), world, args.balance)
         A = full.row_slice(int(bounds[rank]), int(bounds[rank + 1]))
         A = lwb.DeviceCsr(A.rows, A.cols, A.row_offsets.clone(), A.col_indices.clone(),
                           A.values.clone())
@@ -634,7 +637,8 @@ def our_arm(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32" if args.dtype == "fp32" else "f64", "data": "synthetic",
         "config": run_config(args, rows_total, nnz_total, world),
-        "notes": {"l2": "inputs > L2 (2.2 GB matrix streamed per step); no flush"},
+        "notes": {"l2": "inputs > L2 (2.2 GB matrix streamed per step); no flush",
+                  **({"row_split": f"{args.balance}-balanced rows (distributed.row_bounds)"} if world > 1 else {})},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
                      "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
                      "kernel": "k_wo_chunk" if sched is lwb.ScheduleKind.MERGE_PATH else args.schedule,

@@ -14,7 +14,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["nnz_balanced_bounds", "shard_of", "power_iteration", "power_iteration_fused",
+__all__ = ["nnz_balanced_bounds", "work_balanced_bounds", "row_bounds", "shard_of", "power_iteration", "power_iteration_fused",
            "power_iteration_graph", "power_iteration_inplace", "chunk_bounds", "RowShard",
            "GatherLayout"]
 
@@ -35,6 +35,34 @@ def nnz_balanced_bounds(row_offsets, parts: int) -> np.ndarray:
     b = np.minimum(b, rows)
     b[0], b[-1] = 0, rows
     return np.maximum.accumulate(b)
+
+
+def work_balanced_bounds(row_offsets, parts: int) -> np.ndarray:
+    """Row boundaries that balance rows + nnz (merge-path items) instead of nnz:
+    the tile coordinates of merge_path_partition(ts, parts) (reference
+    schedules.py:88-110), i.e. the work_oriented schedule applied across GPUs.
+    A shard's SpMV costs about one item per row plus one per atom, so a shard of
+    many short or empty rows (R-MAT's high row ids; the tail of a degree-sorted
+    operator) is no longer the slowest one. Rows stay whole."""
+    from .schedules import merge_path_partition
+    from .work import TileSet
+
+    off = np.asarray(row_offsets, dtype=np.int64)
+    if parts < 1:
+        raise ValueError("parts must be >= 1")
+    b = merge_path_partition(TileSet(off), parts)[:, 0].astype(np.int64)
+    b[0], b[-1] = 0, off.size - 1
+    return np.maximum.accumulate(b)
+
+
+def row_bounds(row_offsets, parts: int, balance: str = "work") -> np.ndarray:
+    """Shard boundaries by ``balance``: "work" (rows + nnz, work_balanced_bounds)
+    or "nnz" (nnz_balanced_bounds, the north star's split)."""
+    if balance == "work":
+        return work_balanced_bounds(row_offsets, parts)
+    if balance == "nnz":
+        return nnz_balanced_bounds(row_offsets, parts)
+    raise ValueError(f"unknown balance {balance!r}")
 
 
 class RowShard:

@@ -184,3 +184,26 @@ def test_gather_layout_positions():
     buf = lay.to_layout(v)
     pad = np.setdiff1d(np.arange(lay.size), lay.pos)
     assert (buf[torch.as_tensor(pad)] == 0).all()
+
+
+def test_work_balanced_bounds_are_merge_path_tiles():
+    """The rows+nnz split is the tile column of the reference merge-path partition
+    (schedules.py:88-110), rows whole, and balances rows + nnz within one row."""
+    from paper_2301_04792_b200.distributed import row_bounds, work_balanced_bounds
+    from paper_2301_04792_b200.schedules import merge_path_partition
+    from paper_2301_04792_b200.work import TileSet
+
+    rng = np.random.default_rng(7)
+    lengths = rng.integers(0, 40, size=5000)
+    lengths[rng.random(5000) < 0.4] = 0
+    off = np.concatenate([[0], np.cumsum(lengths)])
+    for parts in (1, 2, 3, 4, 8, 13):
+        b = work_balanced_bounds(off, parts)
+        assert b[0] == 0 and b[-1] == off.size - 1 and (np.diff(b) >= 0).all()
+        np.testing.assert_array_equal(b[1:-1], merge_path_partition(TileSet(off), parts)[1:-1, 0])
+        items = (off[b[1:]] + b[1:]) - (off[b[:-1]] + b[:-1])
+        assert items.max() - items.min() <= 2 * (lengths.max() + 1) + 2
+        np.testing.assert_array_equal(row_bounds(off, parts, "work"), b)
+        np.testing.assert_array_equal(row_bounds(off, parts, "nnz"), nnz_balanced_bounds(off, parts))
+    with pytest.raises(ValueError):
+        row_bounds(off, 2, "rows")
