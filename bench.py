@@ -78,8 +78,9 @@ def parse():
                          "chunk's SpMV (0 = 4 when N > 1, else 1)")
     ap.add_argument("--items", type=int, default=0,
                     help="work_oriented items per lane (0 = library default)")
-    ap.add_argument("--balance", default="work", choices=["work", "nnz"],
-                    help="N > 1 row split: rows+nnz balanced (merge-path tiles, default) or nnz balanced")
+    ap.add_argument("--balance", default="cost", choices=["cost", "work", "nnz"],
+                    help="N > 1 row split: nnz + 1.75 rows (measured shard cost, default), rows + nnz "
+                         "(merge-path tiles) or nnz balanced (distributed.row_bounds)")
     ap.add_argument("--relabel", default="on", choices=["on", "off"],
                     help="power mode: symmetric degree relabeling of the C5 operator (one-time)")
     ap.add_argument("--no-fp64", action="store_true", help="skip the fp64 C3 leg")

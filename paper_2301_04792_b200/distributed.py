@@ -14,7 +14,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["nnz_balanced_bounds", "work_balanced_bounds", "row_bounds", "shard_of", "power_iteration", "power_iteration_fused",
+__all__ = ["nnz_balanced_bounds", "work_balanced_bounds", "weighted_bounds", "row_bounds", "shard_of", "power_iteration", "power_iteration_fused",
            "power_iteration_graph", "power_iteration_inplace", "chunk_bounds", "RowShard",
            "GatherLayout"]
 
@@ -55,13 +55,44 @@ def work_balanced_bounds(row_offsets, parts: int) -> np.ndarray:
     return np.maximum.accumulate(b)
 
 
-def row_bounds(row_offsets, parts: int, balance: str = "work") -> np.ndarray:
-    """Shard boundaries by ``balance``: "work" (rows + nnz, work_balanced_bounds)
-    or "nnz" (nnz_balanced_bounds, the north star's split)."""
+def weighted_bounds(row_offsets, parts: int, row_weight: float) -> np.ndarray:
+    """Row boundaries balancing nnz + row_weight * rows (whole rows)."""
+    off = np.asarray(row_offsets, dtype=np.int64)
+    if parts < 1:
+        raise ValueError("parts must be >= 1")
+    rows = off.size - 1
+    cost = off.astype(np.float64) + row_weight * np.arange(rows + 1, dtype=np.float64)
+    targets = cost[-1] * np.arange(parts + 1, dtype=np.float64) / parts
+    b = np.searchsorted(cost, targets, side="left").astype(np.int64)
+    b = np.minimum(b, rows)
+    b[0], b[-1] = 0, rows
+    return np.maximum.accumulate(b)
+
+
+# Measured cost of one row relative to one atom in a shard's work_oriented SpMV
+# step (least squares over per-shard times of C3 at 1-8 shards, B200: 3.4 us per
+# M atoms, 5.9 us per M rows; tools/shard_projection.py, DESIGN.md §6).
+ROW_COST = 1.75
+
+
+def row_bounds(row_offsets, parts: int, balance: str = "cost") -> np.ndarray:
+    """Shard boundaries by ``balance``: "cost" (nnz + ROW_COST * rows, the
+    measured per-shard cost; default), "work" (rows + nnz, the merge-path tiles,
+    work_balanced_bounds), "nnz" (nnz_balanced_bounds, the north star's split) or
+    "w<float>" (nnz + w * rows)."""
+    if balance == "cost":
+        return weighted_bounds(row_offsets, parts, ROW_COST)
     if balance == "work":
         return work_balanced_bounds(row_offsets, parts)
     if balance == "nnz":
         return nnz_balanced_bounds(row_offsets, parts)
+    if balance.startswith("w"):
+        try:
+            w = float(balance[1:])
+        except ValueError:
+            w = None
+        if w is not None and w >= 0:
+            return weighted_bounds(row_offsets, parts, w)
     raise ValueError(f"unknown balance {balance!r}")
 
 

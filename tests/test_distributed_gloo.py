@@ -205,5 +205,10 @@ def test_work_balanced_bounds_are_merge_path_tiles():
         assert items.max() - items.min() <= 2 * (lengths.max() + 1) + 2
         np.testing.assert_array_equal(row_bounds(off, parts, "work"), b)
         np.testing.assert_array_equal(row_bounds(off, parts, "nnz"), nnz_balanced_bounds(off, parts))
+        c = row_bounds(off, parts)   # default: nnz + ROW_COST * rows
+        cost = off + 1.75 * np.arange(off.size)
+        per = cost[c[1:]] - cost[c[:-1]]
+        assert c[0] == 0 and c[-1] == off.size - 1 and (np.diff(c) >= 0).all()
+        assert per.max() - per.min() <= 2 * (lengths.max() + 1.75) + 1e-9
     with pytest.raises(ValueError):
         row_bounds(off, 2, "rows")

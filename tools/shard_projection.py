@@ -73,12 +73,13 @@ def run(name, full, relabel=False, balance="work"):
 
 def main():
     A = lw.generate_rmat_csr(24, 16, seed=3)
-    for bal in ("nnz", "work"):
+    bals = sys.argv[sys.argv.index("--balances") + 1].split(",") if "--balances" in sys.argv else ["nnz", "work"]
+    for bal in bals:
         run("rmat24-ef16-seed3 (C3)", A, balance=bal)
     del A
     if "--c5" in sys.argv:
         A = lw.generate_rmat_csr(26, 16, seed=5).degree_relabel().matrix
-        for bal in ("nnz", "work"):
+        for bal in bals:
             run("rmat26-ef16-seed5 (C5 operator, relabeled)", A, balance=bal)
 
 
