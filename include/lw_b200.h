@@ -123,7 +123,11 @@ int lw_spmv_thread_mapped(const lw_csr_t* A, const void* x, void* y, int64_t lan
 /* work_oriented (merge-path): even share of rows+nnz per lane, carries fixed up
  * in lane order on the device. Replaces _fast.spmv_merge_path (_fast.py:31-52)
  * plus the host partition (kernels.py:81) and the serial carry fix-up
- * (kernels.py:90-91). lanes = 0 selects lw_auto_lanes(). */
+ * (kernels.py:90-91). lanes = 0 selects lw_auto_lanes(). The SpMV and fix-up
+ * kernels are programmatic dependent launches of the kernel before them (they
+ * wait for its results on the device); to the caller the call is ordinary
+ * stream-ordered work: it starts after everything queued before it and
+ * everything queued after it sees its y. */
 size_t lw_spmv_work_oriented_workspace(int64_t rows, int64_t nnz, int64_t lanes,
                                        int32_t dtype);
 int lw_spmv_work_oriented(const lw_csr_t* A, const void* x, void* y, int64_t lanes,
