@@ -326,8 +326,13 @@ __device__ __forceinline__ bool gb_staged_block(OffT cnt, int tc, int NT_) {
     return n_ge == 0 || n_ge * 4 >= tc || tc < 8;
 }
 
-#ifndef LW_GB_MINB   // resident CTAs the fused kernel's registers must allow (A/B; 1 = free)
-#define LW_GB_MINB 1
+// Resident 256-thread CTAs the fused kernel's registers must allow (scaled by
+// 256/NT): 6 -> 40 registers, no spills, 75% occupancy instead of 50% at 64.
+// Block tile, fp32 / fp64: C2b 0.105 -> 0.077 / 0.151 -> 0.100 ms, C2u 0.182 ->
+// 0.170 / 0.214 -> 0.182, C3 11.6 -> 8.4 / 13.1 -> 9.9 ms; power-law fp64 at
+// skew <= 1.2 +1-3%. (5 -> 48 registers: C2b 0.087; 8 -> 32 registers spills.)
+#ifndef LW_GB_MINB
+#define LW_GB_MINB 6
 #endif
 template <class OffT, class ValT, int NT, bool PROBE, int MODE = GB_ALL>
 __global__ void __launch_bounds__(NT, MODE == GB_FUSED ? LW_GB_MINB * 256 / NT : 1)
