@@ -267,8 +267,15 @@ __global__ void k_spmm_carry_fixup(const int64_t* __restrict__ carry_tile,
 // identical and, for fp64 data, bit-identical to the reference — no atomics,
 // no zeroing pass.
 constexpr int GT_U = 4;   // atoms per residue batch (loads in flight)
+// Resident MM_NT-thread CTAs the group-tile kernel's registers must allow: 4 ->
+// 64 registers (73 uncapped), fp32 n = 4 / 16 / 64: C2u 0.286 / 0.719 / 2.71 ->
+// 0.275 / 0.600 / 2.18 ms, C2b 0.245 / 0.497 / 1.96 -> 0.249 / 0.431 / 1.66, C3
+// -1..-3%. (5 -> 48 registers spills 60-92 B.)
+#ifndef LW_MM_GT_MINB
+#define LW_MM_GT_MINB 4
+#endif
 template <class OffT, class ValT, int VEC>
-__global__ void __launch_bounds__(MM_NT)
+__global__ void __launch_bounds__(MM_NT, LW_MM_GT_MINB)
     k_spmm_group_tiles(Csr<OffT, ValT> A, const ValT* __restrict__ B, ValT* __restrict__ C, int64_t n,
                        int64_t lanes, int64_t gs, int64_t tpb, int lg_ts) {
     const int64_t gt = (int64_t)blockIdx.x * MM_NT + threadIdx.x;
