@@ -370,7 +370,9 @@ def power_measure(args, world, rank, local, dev, scale, seed):
 
         torch.cuda.synchronize()
         t_l = time.perf_counter()
-        layout = GatherLayout(bounds, chunks)
+        # exact (unpadded) layout over NCCL: uneven per-rank pieces, no padding
+        exact = world > 1 and dist.get_backend() == "nccl"
+        layout = GatherLayout(bounds, chunks, exact=exact)
         A = layout.remap_columns(A)
         pos_t = layout.pos_on(dev)
         # buffer form -> original numbering in one gather (relabel composed in)
@@ -456,8 +458,12 @@ def power_measure(args, world, rank, local, dev, scale, seed):
                    "fused_allgather": bool(args.fused), "cuda_graph": bool(args.graph),
                    "x_layout": ("degree-relabeled P A P^T (DESIGN.md 4f)" if relabel else "as generated")
                                + (" + hot-x packed (DESIGN.md 4e)" if hot else ""),
-                   "gather": ("in-place all-gather layout" if layout is not None else
+                   "gather": (("exact in-place all-gather (uneven pieces)" if layout.exact else
+                               "in-place all-gather layout") if layout is not None else
                               "fused into the SpMV row stores" if args.fused else "CUDA graph")},
+        "allgather_mb_per_gpu_per_iter": (None if layout is None or world == 1 else round(
+            ((layout.size - shard.rows) if layout.exact else (layout.size - sum(layout.widths)))
+            * A.values.element_size() / 1e6, 1)),
         "one_time_prep_ms": prep_ms,
         "breakdown_ms": None if (args.fused or args.graph) else {"spmv_max_rank": round(spmv_ms, 3),
                                                  "allgather_normalise": round(ms - spmv_ms, 3)},

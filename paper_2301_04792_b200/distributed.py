@@ -143,12 +143,26 @@ class GatherLayout:
     in place, the norm and the scaling run over the buffer (padding stays 0) —
     no send copy, concatenation or reorder pass per iteration."""
 
-    def __init__(self, bounds, chunks: int = 1):
+    def __init__(self, bounds, chunks: int = 1, exact: bool = False):
         b = np.asarray(bounds, dtype=np.int64)
         self.world = b.size - 1
         self.chunks = max(1, int(chunks))
+        self.bounds = b
         counts = np.diff(b)
         self.cb = [chunk_bounds(int(c), self.chunks) for c in counts]
+        # exact: no padding — the buffer is the vector itself (pos = identity) and
+        # chunk k is exchanged as uneven per-rank pieces (NCCL's all_gather with
+        # uneven outputs: one broadcast per rank, grouped), so a shard with many
+        # more rows than the others (R-MAT's sparse tail; the degree-sorted C5
+        # operator puts 86% of the rows on the last of 8 shards) costs no padding
+        self.exact = bool(exact)
+        if self.exact:
+            self.widths = [0] * self.chunks
+            self.offs = np.zeros(self.chunks + 1, dtype=np.int64)
+            self.size = int(b[-1])
+            self.pos = np.arange(self.size, dtype=np.int64)
+            self._pos_dev = {}
+            return
         self.widths = [max(int(self.cb[r][k + 1] - self.cb[r][k]) for r in range(self.world))
                        for k in range(self.chunks)]
         self.offs = np.concatenate([[0], np.cumsum([self.world * w for w in self.widths])]).astype(np.int64)
@@ -173,14 +187,51 @@ class GatherLayout:
 
     def slot(self, rank: int, k: int) -> tuple[int, int, int, int]:
         """(buffer start of my slot, slot width, local row range r0, r1) of chunk k."""
-        return (int(self.offs[k] + rank * self.widths[k]), self.widths[k],
-                int(self.cb[rank][k]), int(self.cb[rank][k + 1]))
+        r0, r1 = int(self.cb[rank][k]), int(self.cb[rank][k + 1])
+        if self.exact:
+            return int(self.bounds[rank]) + r0, r1 - r0, r0, r1
+        return int(self.offs[k] + rank * self.widths[k]), self.widths[k], r0, r1
+
+    def pieces(self, k: int) -> list[tuple[int, int]]:
+        """exact layout: (start, length) of chunk k of every rank in the vector."""
+        return [(int(self.bounds[r] + self.cb[r][k]), int(self.cb[r][k + 1] - self.cb[r][k]))
+                for r in range(self.world)]
+
+    def exchange(self, buf, k: int, rank: int, group=None):
+        """Async all-gather of chunk k into ``buf`` in place; returns the work."""
+        import torch
+        import torch.distributed as dist
+
+        if not self.exact:
+            lo, hi = int(self.offs[k]), int(self.offs[k + 1])
+            start = int(self.offs[k] + rank * self.widths[k])
+            return dist.all_gather_into_tensor(buf[lo:hi], buf[start:start + self.widths[k]], group=group,
+                                               async_op=True)
+        views = [buf[a:a + n] for a, n in self.pieces(k)]
+        if dist.get_backend(group) == "nccl":   # uneven outputs: grouped broadcasts, exact bytes
+            return dist.all_gather(views, views[rank], group=group, async_op=True)
+        # (gloo only gathers equal sizes: pad through a staging buffer — tests)
+        w = max(n for _, n in self.pieces(k)) if self.world else 0
+        tmp = torch.zeros(self.world * w, dtype=buf.dtype, device=buf.device)
+        mine = torch.zeros(w, dtype=buf.dtype, device=buf.device)
+        mine[: views[rank].numel()].copy_(views[rank])
+        dist.all_gather_into_tensor(tmp, mine, group=group)
+        for r, v in enumerate(views):
+            v.copy_(tmp[r * w: r * w + v.numel()])
+
+        class _Done:
+            def wait(self):
+                return None
+
+        return _Done()
 
     def remap_columns(self, m):
         """The operator with column c renamed pos[c] (host CsrMatrix or DeviceCsr);
         its column count becomes the buffer size."""
         from .sparse import CsrMatrix
 
+        if self.exact:   # pos is the identity
+            return m
         if isinstance(m, CsrMatrix):
             return CsrMatrix(m.rows, self.size, m.row_offsets, self.pos[m.col_indices], m.values)
         import torch
@@ -237,9 +288,7 @@ def power_iteration_inplace(local_spmv, layout: GatherLayout, iters: int, rank: 
             start, width, r0, r1 = layout.slot(rank, k)
             local_spmv(x, r0, r1, nxt[start:start + (r1 - r0)])
             if world > 1:
-                lo, hi = int(layout.offs[k]), int(layout.offs[k + 1])
-                works.append(dist.all_gather_into_tensor(nxt[lo:hi], nxt[start:start + width],
-                                                         group=group, async_op=True))
+                works.append(layout.exchange(nxt, k, rank, group))
         for w in works:
             w.wait()
         nrm = _normalise_into(nxt)

@@ -123,7 +123,7 @@ def test_chunked_single_process_equals_plain():
     np.testing.assert_allclose(n4, n1, rtol=1e-12)
 
 
-def _worker_inplace(rank, world, port, out, chunks):
+def _worker_inplace(rank, world, port, out, chunks, exact=False):
     """The in-place gather layout: operator columns renamed into the gather
     buffer, SpMV writing its slot, all-gather in place, norm + scale in place."""
     from oracle import oracle
@@ -134,7 +134,7 @@ def _worker_inplace(rank, world, port, out, chunks):
     try:
         m = lw.generate_power_law_csr(4000, 10.0, 1.2, seed=7)
         b = nnz_balanced_bounds(m.row_offsets, world)
-        lay = GatherLayout(b, chunks)
+        lay = GatherLayout(b, chunks, exact=exact)
         mine = lay.remap_columns(shard_of(m, b, rank))
 
         def local(x, r0, r1, out_view):
@@ -148,14 +148,18 @@ def _worker_inplace(rank, world, port, out, chunks):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,chunks", [(2, 1), (2, 3), (3, 2)])
-def test_inplace_gather_layout_matches_single_process(world, chunks):
+@pytest.mark.parametrize("world,chunks,exact", [(2, 1, False), (2, 3, False), (3, 2, False), (2, 1, True),
+                                                (3, 2, True)])
+def test_inplace_gather_layout_matches_single_process(world, chunks, exact):
+    """Padded slots (equal-size NCCL all-gather) and the exact layout (uneven
+    per-rank pieces; gloo emulates NCCL's uneven all_gather through a padded
+    staging buffer) give the single-process iterates."""
     from oracle import oracle
 
     port = _free_port()
     mgr = mp.get_context("spawn").Manager()
     out = mgr.dict()
-    mp.start_processes(_worker_inplace, args=(world, port, out, chunks), nprocs=world, join=True,
+    mp.start_processes(_worker_inplace, args=(world, port, out, chunks, exact), nprocs=world, join=True,
                        start_method="spawn")
     m = lw.generate_power_law_csr(4000, 10.0, 1.2, seed=7)
     x = np.full(m.rows, 1.0 / np.sqrt(m.rows))
@@ -184,6 +188,18 @@ def test_gather_layout_positions():
     buf = lay.to_layout(v)
     pad = np.setdiff1d(np.arange(lay.size), lay.pos)
     assert (buf[torch.as_tensor(pad)] == 0).all()
+
+
+def test_exact_gather_layout_is_the_vector():
+    from paper_2301_04792_b200.distributed import GatherLayout
+
+    b = np.array([0, 5, 12, 13])
+    lay = GatherLayout(b, chunks=2, exact=True)
+    assert lay.size == 13 and (lay.pos == np.arange(13)).all()
+    assert lay.pieces(0) == [(0, 2), (5, 3), (12, 0)] and lay.pieces(1) == [(2, 3), (8, 4), (12, 1)]
+    assert lay.slot(1, 1) == (8, 4, 3, 7)
+    m = lw.generate_power_law_csr(50, 4.0, 1.5, seed=1)
+    assert lay.remap_columns(m) is m
 
 
 def test_work_balanced_bounds_are_merge_path_tiles():
