@@ -372,8 +372,11 @@ def power_iteration(local_spmv, n: int, shard: RowShard, iters: int, group=None,
     ``chunks > 1`` it is called as ``local_spmv(x_full, r0, r1)`` for local row
     ranges and must return those rows.
 
+    Over NCCL with uneven shards the exchange is exact: each rank's rows (per
+    chunk) go out as one piece of an uneven all_gather straight into the full y
+    (grouped broadcasts, no padding). Otherwise (gloo, even shards):
     chunks == 1: the uneven shards are padded to the largest shard so one
-    all_gather_into_tensor (NCCL over NVLink) moves them.
+    all_gather_into_tensor moves them.
     chunks > 1: the shard is cut into row chunks (every rank uses the same count,
     so chunk k of every rank is exchanged together); chunk k's all-gather is
     issued asynchronously as soon as its SpMV is enqueued, so it runs on NCCL's
@@ -412,9 +415,28 @@ def power_iteration(local_spmv, n: int, shard: RowShard, iters: int, group=None,
             idx = np.concatenate([offs[k] + r * widths[k] + np.arange(cb[r][k + 1] - cb[r][k])
                                   for r in range(world) for k in range(chunks)]).astype(np.int64)
             order = torch.as_tensor(idx, device=x.device)
+    # NCCL gathers uneven pieces exactly (grouped broadcasts): no padding, y
+    # assembled in row order in place (GatherLayout's exact mode, without the layout)
+    exact = world > 1 and dist.get_backend(group) == "nccl" and not even
+    if exact:
+        y_full = torch.empty(n, dtype=x.dtype, device=x.device)
+        b = shard.bounds
+        cbs = [chunk_bounds(int(c), chunks) for c in counts]
+        views = [[y_full[int(b[r] + cbs[r][c]): int(b[r] + cbs[r][c + 1])] for r in range(world)]
+                 for c in range(chunks)]
     norms = []
     for k in range(iters):
-        if chunks == 1:
+        if exact:
+            works = []
+            for c in range(chunks):
+                mine_c = views[c][shard.rank]
+                r0 = int(cbs[shard.rank][c])
+                mine_c.copy_(local_spmv(x, r0, r0 + mine_c.numel()) if chunks > 1 else local_spmv(x))
+                works.append(dist.all_gather(views[c], mine_c, group=group, async_op=True))
+            for w in works:
+                w.wait()
+            y = y_full
+        elif chunks == 1:
             y_local = local_spmv(x)
             if world > 1:
                 send[: shard.rows].copy_(y_local)
