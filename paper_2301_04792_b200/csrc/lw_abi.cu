@@ -10,7 +10,7 @@ namespace lw {
 int spmv_thread_mapped(const lw_csr_t*, const void*, void*, int64_t, const lw_probe_t*, cudaStream_t);
 int spmv_work_oriented(const lw_csr_t*, const void*, void*, int64_t, void*, size_t, const lw_probe_t*, unsigned, cudaStream_t);
 int spmv_group_mapped(const lw_csr_t*, const void*, void*, int64_t, int64_t, int64_t, const lw_probe_t*, cudaStream_t);
-size_t wo_workspace(int64_t rows, int64_t nnz, int64_t lanes);
+size_t wo_workspace(int64_t rows, int64_t nnz, int64_t lanes, int dtype);
 int64_t wo_lanes(int64_t rows, int64_t nnz, int64_t lanes);
 int64_t group_auto_lanes(int64_t rows, int64_t gs, int64_t tpb);
 int merge_path_partition(int64_t, int64_t, const void*, int, int64_t, int64_t*, cudaStream_t);
@@ -147,9 +147,8 @@ int lw_spmv_thread_mapped(const lw_csr_t* A, const void* x, void* y, int64_t lan
 }
 
 size_t lw_spmv_work_oriented_workspace(int64_t rows, int64_t nnz, int64_t lanes, int32_t dtype) {
-    (void)dtype;
-    if (rows < 0 || nnz < 0 || lanes < 0) return 0;
-    return wo_workspace(rows, nnz, lanes);
+    if (rows < 0 || nnz < 0 || lanes < 0 || (dtype != LW_F32 && dtype != LW_F64)) return 0;
+    return wo_workspace(rows, nnz, lanes, dtype);   // fp64 lanes hold more (smaller) chunks
 }
 
 int lw_spmv_work_oriented(const lw_csr_t* A, const void* x, void* y, int64_t lanes, void* ws,

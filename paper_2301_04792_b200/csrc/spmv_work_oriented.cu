@@ -27,8 +27,9 @@
 
 namespace lw {
 
-// Chunk geometry shared by every dtype: a chunk is at most WO_S merge-path items
-// (rows + atoms) and its atoms sit in an 8-aligned window of WO_W atoms.
+// Lane geometry (every dtype) and fp32 chunk geometry: a chunk is at most WO_S
+// merge-path items (rows + atoms) and its atoms sit in an 8-aligned window of
+// WO_W atoms (fp64 chunks are smaller, WoCfg<double>).
 #ifndef LW_WO_W
 #define LW_WO_W 4096
 #endif
@@ -54,17 +55,35 @@ struct WoCfg;
 // allocator otherwise lands at 46-58). fp32 is left uncapped: it lands at 32
 // (4 x 512, full occupancy) by itself, and a __maxnreg__(32) changes its code
 // generation for the worse (0.992 -> 1.005 ms packed on C3).
+// W / S: the dtype's chunk window (atoms) and chunk size (merge-path items). The
+// LANE geometry stays WO_S for every dtype (lw_auto_lanes, probes and imbalance
+// do not depend on the value type); fp64 cuts each lane into chunks of a 2048-atom
+// window run by 256 threads (its 40-register, 3 x 512-thread geometry at 4096
+// measured 1.349 ms on C3, 2048 x 256 1.30).
 template <>
 struct WoCfg<float> {
     static constexpr int NT = LW_WO_NT, IPT = WO_W / LW_WO_NT, MAXR = 0;   // uncapped
+    static constexpr int W = WO_W, S = WO_S;
 };
 #ifndef LW_WO_MAXR64
 #define LW_WO_MAXR64 40
 #endif
+#ifndef LW_WO_W64
+#define LW_WO_W64 2048
+#endif
+#ifndef LW_WO_NT64
+#define LW_WO_NT64 256
+#endif
 template <>
 struct WoCfg<double> {
-    static constexpr int NT = LW_WO_NT, IPT = WO_W / LW_WO_NT, MAXR = LW_WO_MAXR64;
+    static constexpr int NT = LW_WO_NT64, IPT = LW_WO_W64 / LW_WO_NT64, MAXR = LW_WO_MAXR64;
+    // S: an exact fraction of the lane's WO_S items (2 chunks per lane at 2048,
+    // none left over), at most W - 8 so the 8-aligned window holds the chunk
+    static constexpr int W = LW_WO_W64, S = WO_S / (WO_W / LW_WO_W64);
 };
+static_assert(WoCfg<double>::S + 8 <= WoCfg<double>::W && WoCfg<double>::S <= WO_S,
+              "fp64 chunks within the lane geometry");
+inline int wo_chunk_items(int dtype) { return dtype == LW_F32 ? WoCfg<float>::S : WoCfg<double>::S; }
 
 // ---- 1. partition ---------------------------------------------------------
 // Boundary b of lane l = b / J, chunk j = b % J sits on diagonal
@@ -129,12 +148,13 @@ struct WoScan {
 
 template <class ValT>
 struct WoSmem {
-    // row ends are window positions (< WO_W = 4096): 16 bits each, which leaves
+    // row ends are window positions (< W <= 4096): 16 bits each, which leaves
     // 32 KB more of each SM's unified L1/shared array to cache x (-8% time on C3)
-    static constexpr size_t end_off = 0;                                   // uint16[WO_S]
-    static constexpr size_t seg_off = (end_off + sizeof(uint16_t) * WO_S + 15) / 16 * 16;  // ValT[WO_W]
-    static constexpr size_t flag_off = seg_off + sizeof(ValT) * WO_W;      // uint32[W/32+2]
-    static constexpr size_t bytes = flag_off + sizeof(uint32_t) * (WO_W / 32 + 2);
+    static constexpr int W = WoCfg<ValT>::W, S = WoCfg<ValT>::S;
+    static constexpr size_t end_off = 0;                                   // uint16[S]
+    static constexpr size_t seg_off = (end_off + sizeof(uint16_t) * S + 15) / 16 * 16;  // ValT[W]
+    static constexpr size_t flag_off = seg_off + sizeof(ValT) * W;         // uint32[W/32+2]
+    static constexpr size_t bytes = flag_off + sizeof(uint32_t) * (W / 32 + 2);
 };
 
 // ---- fused all-gather output (power iteration over NVLink) -------------------------
@@ -305,12 +325,12 @@ __device__ __forceinline__ void wo_chunk_body(Csr<OffT, ValT> A, const ValT* __r
                                               int64_t* __restrict__ carry_tile, double* __restrict__ carry_val,
                                               Probe probe, PeerOut po, const ValT* __restrict__ xh) {
     constexpr int NT = WoCfg<ValT>::NT, IPT = WoCfg<ValT>::IPT;
-    constexpr int W = WO_W, S = WO_S;
+    constexpr int W = WoCfg<ValT>::W, S = WoCfg<ValT>::S;
     static_assert(NT * IPT == W, "window must be NT*IPT atoms");
     using SM = WoSmem<ValT>;
     extern __shared__ __align__(16) unsigned char sm[];
     uint16_t* s_end = reinterpret_cast<uint16_t*>(sm + SM::end_off);
-    static_assert(WO_W <= 65536, "window positions must fit 16 bits");
+    static_assert(W <= 65536, "window positions must fit 16 bits");
     ValT* s_seg = reinterpret_cast<ValT*>(sm + SM::seg_off);
     uint32_t* s_flag = reinterpret_cast<uint32_t*>(sm + SM::flag_off);
     __shared__ WoScan<NT> scan;
@@ -711,13 +731,15 @@ struct WoPlan {
     int64_t total, lanes, items, J;
 };
 
-static WoPlan wo_plan(int64_t rows, int64_t nnz, int64_t lanes) {
+// lanes: the schedule's (auto: one WO_S-item lane per chunk of the fp32 geometry,
+// for every dtype); J: chunks of at most `chunk` items per lane (the dtype's S)
+static WoPlan wo_plan(int64_t rows, int64_t nnz, int64_t lanes, int64_t chunk = WO_S) {
     WoPlan p{};
     p.total = rows + nnz;
     if (lanes <= 0) lanes = p.total > 0 ? ceil_div(p.total, WO_S) : 1;
     p.lanes = lanes;
     p.items = p.total > 0 ? ceil_div(p.total, lanes) : 0;
-    p.J = p.items > 0 ? ceil_div(p.items, WO_S) : 1;
+    p.J = p.items > 0 ? ceil_div(p.items, chunk) : 1;
     return p;
 }
 
@@ -759,8 +781,8 @@ static WoWs wo_ws(const WoPlan& p, void* ws) {
     return r;
 }
 
-size_t wo_workspace(int64_t rows, int64_t nnz, int64_t lanes) {
-    const WoPlan p = wo_plan(rows, nnz, lanes);
+size_t wo_workspace(int64_t rows, int64_t nnz, int64_t lanes, int dtype) {
+    const WoPlan p = wo_plan(rows, nnz, lanes, wo_chunk_items(dtype));
     const size_t nb = (size_t)(p.lanes * p.J + 1), nc = wo_carries(p);
     return align_up(nb * 8, 256) + 2 * align_up(nc * 8, 256) + wo_fix_bytes(p);
 }
@@ -866,11 +888,11 @@ static int launch_wo(const lw_csr_t* A, const void* x, void* y, const WoPlan& p,
         const unsigned nsb = (unsigned)ceil_div((int64_t)nb, 256);
         const unsigned npb = (unsigned)ceil_div(n_hot, 256);
         k_search_pack<OffT, ValT><<<nsb + npb, 256, 0, s>>>(a.off, a.rows, a.nnz, (int64_t)nb, p.J, p.items,
-                                                          WO_S, tiles, nsb, (const ValT*)x, hot_cols,
+                                                          WoCfg<ValT>::S, tiles, nsb, (const ValT*)x, hot_cols,
                                                           n_hot, xh, W.ticket);
         LW_LAUNCH_CHECK();
     } else if (phases & WO_PHASE_PARTITION) {
-        int rc = launch_search<OffT>(a.off, a.rows, a.nnz, (int64_t)nb, p.J, p.items, WO_S, tiles,
+        int rc = launch_search<OffT>(a.off, a.rows, a.nnz, (int64_t)nb, p.J, p.items, WoCfg<ValT>::S, tiles,
                                      nullptr, s, W.ticket);
         if (rc) return rc;
     }
@@ -910,7 +932,7 @@ static int launch_wo_peers(const lw_csr_t* A, const void* x, void* y, const WoPl
     int64_t* c_tile = W.c_tile;
     double* c_val = W.c_val;
     if (p.lanes > 0x7fffffff) return LW_E_UNSUPPORTED;
-    int rc = launch_search<OffT>(a.off, a.rows, a.nnz, (int64_t)nb, p.J, p.items, WO_S, tiles, nullptr, s,
+    int rc = launch_search<OffT>(a.off, a.rows, a.nnz, (int64_t)nb, p.J, p.items, WoCfg<ValT>::S, tiles, nullptr, s,
                                  W.ticket);
     if (rc) return rc;
     const bool vec = ((uintptr_t)A->col_indices % 32 == 0) && ((uintptr_t)A->values % 32 == 0);
@@ -945,11 +967,11 @@ int spmv_work_oriented_peers(const lw_csr_t* A, const void* x, void* y, int64_t 
     if (n_peers < 0 || n_peers > LW_MAX_PEERS || (n_peers > 0 && !peer_ptrs) || row_base < 0 ||
         n_hot < 0 || (n_hot > 0 && !hot_cols))
         return LW_E_INVALID_ARG;
-    const WoPlan p = wo_plan(A->rows, A->nnz, lanes);
+    const WoPlan p = wo_plan(A->rows, A->nnz, lanes, wo_chunk_items(A->dtype));
     if (A->rows == 0) return LW_OK;
     const bool hot = hot_cols != nullptr || n_hot > 0;
     const size_t need = hot ? wo_hotx_workspace(A->rows, A->nnz, lanes, n_hot, A->dtype)
-                            : wo_workspace(A->rows, A->nnz, lanes);
+                            : wo_workspace(A->rows, A->nnz, lanes, A->dtype);
     if (!ws || ws_bytes < need) return LW_E_WORKSPACE;
     PeerOut po{};
     po.n = n_peers;
@@ -975,9 +997,9 @@ int spmv_work_oriented_peers(const lw_csr_t* A, const void* x, void* y, int64_t 
 int spmv_work_oriented(const lw_csr_t* A, const void* x, void* y, int64_t lanes, void* ws,
                        size_t ws_bytes, const lw_probe_t* probe, unsigned phases,
                        cudaStream_t s) {
-    const WoPlan p = wo_plan(A->rows, A->nnz, lanes);
+    const WoPlan p = wo_plan(A->rows, A->nnz, lanes, wo_chunk_items(A->dtype));
     if (A->rows == 0) return LW_OK;
-    if (!ws || ws_bytes < wo_workspace(A->rows, A->nnz, lanes)) return LW_E_WORKSPACE;
+    if (!ws || ws_bytes < wo_workspace(A->rows, A->nnz, lanes, A->dtype)) return LW_E_WORKSPACE;
     const bool o32 = A->offset_bits == 32;
     if (A->dtype == LW_F32)
         return o32 ? launch_wo<int32_t, float>(A, x, y, p, ws, probe, phases, s)
@@ -989,14 +1011,14 @@ int spmv_work_oriented(const lw_csr_t* A, const void* x, void* y, int64_t lanes,
 // Workspace of the hot-x variant: the plain one plus the packed hot values.
 size_t wo_hotx_workspace(int64_t rows, int64_t nnz, int64_t lanes, int64_t n_hot, int dtype) {
     // at least one slot: atoms outside a chunk's window read (and discard) slot 0
-    return wo_workspace(rows, nnz, lanes) + align_up((size_t)(n_hot > 0 ? n_hot : 1) * (dtype == LW_F32 ? 4 : 8), 256);
+    return wo_workspace(rows, nnz, lanes, dtype) + align_up((size_t)(n_hot > 0 ? n_hot : 1) * (dtype == LW_F32 ? 4 : 8), 256);
 }
 
 int spmv_work_oriented_hotx(const lw_csr_t* A, const int32_t* hot_cols, int32_t n_hot,
                             const void* x, void* y, int64_t lanes, void* ws, size_t ws_bytes,
                             unsigned phases, cudaStream_t s) {
     if (n_hot < 0 || (n_hot > 0 && !hot_cols)) return LW_E_INVALID_ARG;
-    const WoPlan p = wo_plan(A->rows, A->nnz, lanes);
+    const WoPlan p = wo_plan(A->rows, A->nnz, lanes, wo_chunk_items(A->dtype));
     if (A->rows == 0) return LW_OK;
     if (!ws || ws_bytes < wo_hotx_workspace(A->rows, A->nnz, lanes, n_hot, A->dtype)) return LW_E_WORKSPACE;
     static const int32_t none = 0;   // any non-null marker selects the hot kernel when n_hot == 0
