@@ -111,8 +111,15 @@ __device__ __forceinline__ void mm_range(const Csr<OffT, ValT>& A, const ValT* _
 }
 
 // ---- thread_mapped: lane l owns tiles l, l+P, ... (_fast.py:80-90) --------------------
+// Resident MM_NT-thread CTAs the thread-mapped kernel's registers must allow: 4 ->
+// 64 registers (80 uncapped for fp32 vectors): fp32 n = 4 / 16 / 64, C3 78 / 117 /
+// 181 -> 61 / 87 / 131 ms, C2u n = 16 / 64 -17 / -19%, C2b n = 16 -12%, n = 4 +-3%.
+// (5 -> 48 registers spills 104 B.)
+#ifndef LW_MM_TM_MINB
+#define LW_MM_TM_MINB 4
+#endif
 template <class OffT, class ValT, int VEC>
-__global__ void __launch_bounds__(MM_NT)
+__global__ void __launch_bounds__(MM_NT, LW_MM_TM_MINB)
     k_spmm_thread_mapped(Csr<OffT, ValT> A, const ValT* __restrict__ B, ValT* __restrict__ C,
                          int64_t n, int64_t lanes, int lg_ts) {
     const int64_t gt = (int64_t)blockIdx.x * MM_NT + threadIdx.x;
