@@ -56,15 +56,27 @@ def work_balanced_bounds(row_offsets, parts: int) -> np.ndarray:
 
 
 def weighted_bounds(row_offsets, parts: int, row_weight: float) -> np.ndarray:
-    """Row boundaries balancing nnz + row_weight * rows (whole rows)."""
+    """Row boundaries balancing nnz + row_weight * rows (whole rows): b_k is the
+    first row whose prefix cost off[t] + w*t reaches k/parts of the total. A
+    vectorised bisection over the parts+1 targets (no rows-sized temporaries:
+    C5's 67 M offsets would need two 0.5 GB cost arrays per rank)."""
     off = np.asarray(row_offsets, dtype=np.int64)
     if parts < 1:
         raise ValueError("parts must be >= 1")
+    if row_weight < 0:
+        raise ValueError("row_weight must be >= 0")
     rows = off.size - 1
-    cost = off.astype(np.float64) + row_weight * np.arange(rows + 1, dtype=np.float64)
-    targets = cost[-1] * np.arange(parts + 1, dtype=np.float64) / parts
-    b = np.searchsorted(cost, targets, side="left").astype(np.int64)
-    b = np.minimum(b, rows)
+    w = float(row_weight)
+    total = float(off[-1]) + w * rows
+    targets = total * np.arange(parts + 1, dtype=np.float64) / parts
+    lo = np.zeros(parts + 1, dtype=np.int64)           # first t with cost(t) >= target
+    hi = np.full(parts + 1, rows, dtype=np.int64)
+    while (lo < hi).any():
+        mid = (lo + hi) // 2
+        ge = off[mid].astype(np.float64) + w * mid >= targets
+        hi = np.where(ge, mid, hi)
+        lo = np.where(ge, lo, mid + 1)
+    b = lo
     b[0], b[-1] = 0, rows
     return np.maximum.accumulate(b)
 
@@ -128,6 +140,16 @@ def chunk_bounds(rows: int, chunks: int) -> np.ndarray:
     """Split local rows [0, rows) into ``chunks`` contiguous, near-equal pieces."""
     chunks = max(1, int(chunks))
     return (np.arange(chunks + 1, dtype=np.int64) * rows) // chunks
+
+
+class _Completed:
+    """A finished exchange (the synchronous gloo emulation) with the async API."""
+
+    def wait(self):
+        return None
+
+
+_DONE = _Completed()
 
 
 class GatherLayout:
@@ -218,12 +240,7 @@ class GatherLayout:
         dist.all_gather_into_tensor(tmp, mine, group=group)
         for r, v in enumerate(views):
             v.copy_(tmp[r * w: r * w + v.numel()])
-
-        class _Done:
-            def wait(self):
-                return None
-
-        return _Done()
+        return _DONE
 
     def remap_columns(self, m):
         """The operator with column c renamed pos[c] (host CsrMatrix or DeviceCsr);
