@@ -44,9 +44,43 @@ def random_csr(rng):
     return off, col, val, x, rows, cols, integer
 
 
+def spmm_sweep(budget, rng):
+    """The same for SpMM (n = 1..70 columns of B) under every schedule."""
+    t_end = time.time() + budget
+    n_cases = n_runs = 0
+    while time.time() < t_end:
+        off, col, val, x, rows, cols, integer = random_csr(rng)
+        n = int(rng.integers(1, 70))
+        B = (rng.integers(-3, 4, size=(cols, n)).astype(np.float64) if integer else rng.random((cols, n)))
+        want = oracle.spmm(off, col, val, B, "thread-mapped", lanes=1)
+        scale = oracle.abs_spmm_sums(off, col, val, B)
+        for dt in (torch.float32, torch.float64):
+            if not integer and dt == torch.float32:
+                continue   # fp32 rounding of B/values: covered by the SpMV sweep's fp32 path
+            m = lw.DeviceCsr(rows, cols, torch.as_tensor(off).cuda().to(torch.int32),
+                             torch.as_tensor(col).cuda().to(torch.int32), torch.as_tensor(val).cuda().to(dt))
+            Bt = torch.as_tensor(B).cuda().to(dt)
+            for cfg in (lw.ExecutorConfig(schedule=K.THREAD_MAPPED), lw.ExecutorConfig(schedule=K.MERGE_PATH),
+                        lw.ExecutorConfig(schedule=K.GROUP_MAPPED, group_size=32),
+                        lw.ExecutorConfig(schedule=K.GROUP_MAPPED, lanes=int(rng.integers(1, 3000)),
+                                          group_size=int(rng.integers(1, 300)),
+                                          tiles_per_block=int(rng.integers(1, 300)))):
+                C = lw.spmm(m, Bt, cfg).double().cpu().numpy()
+                ok = np.array_equal(C, want) if integer else oracle.tolerance_ok(C, want, scale, 1e-12)[0]
+                n_runs += 1
+                if not ok:
+                    print("SPMM MISMATCH", dict(rows=rows, cols=cols, n=n, dtype=str(dt), cfg=str(cfg)), flush=True)
+                    return 1
+        n_cases += 1
+    print(f"spmm fuzz ok: {n_cases} matrices, {n_runs} SpMMs", flush=True)
+    return 0
+
+
 def main():
     budget = float(sys.argv[1]) if len(sys.argv) > 1 else 120.0
     rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
+    if "--spmm" in sys.argv:
+        return spmm_sweep(budget, rng)
     t_end = time.time() + budget
     n_cases = n_runs = 0
     while time.time() < t_end:
