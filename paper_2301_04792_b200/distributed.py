@@ -150,6 +150,7 @@ class _Completed:
 
 
 _DONE = _Completed()
+_UNEVEN_OK = [True]   # cleared if the NCCL backend rejects an uneven all_gather
 
 
 class GatherLayout:
@@ -230,9 +231,12 @@ class GatherLayout:
             return dist.all_gather_into_tensor(buf[lo:hi], buf[start:start + self.widths[k]], group=group,
                                                async_op=True)
         views = [buf[a:a + n] for a, n in self.pieces(k)]
-        if dist.get_backend(group) == "nccl":   # uneven outputs: grouped broadcasts, exact bytes
-            return dist.all_gather(views, views[rank], group=group, async_op=True)
-        # (gloo only gathers equal sizes: pad through a staging buffer — tests)
+        if dist.get_backend(group) == "nccl" and _UNEVEN_OK[0]:   # grouped broadcasts, exact bytes
+            try:
+                return dist.all_gather(views, views[rank], group=group, async_op=True)
+            except (RuntimeError, ValueError):   # a build without uneven all_gather: pad instead
+                _UNEVEN_OK[0] = False
+        # (gloo only gathers equal sizes: pad through a staging buffer)
         w = max(n for _, n in self.pieces(k)) if self.world else 0
         tmp = torch.zeros(self.world * w, dtype=buf.dtype, device=buf.device)
         mine = torch.zeros(w, dtype=buf.dtype, device=buf.device)
@@ -434,7 +438,7 @@ def power_iteration(local_spmv, n: int, shard: RowShard, iters: int, group=None,
             order = torch.as_tensor(idx, device=x.device)
     # NCCL gathers uneven pieces exactly (grouped broadcasts): no padding, y
     # assembled in row order in place (GatherLayout's exact mode, without the layout)
-    exact = world > 1 and dist.get_backend(group) == "nccl" and not even
+    exact = world > 1 and dist.get_backend(group) == "nccl" and not even and _UNEVEN_OK[0]
     if exact:
         y_full = torch.empty(n, dtype=x.dtype, device=x.device)
         b = shard.bounds
@@ -449,7 +453,17 @@ def power_iteration(local_spmv, n: int, shard: RowShard, iters: int, group=None,
                 mine_c = views[c][shard.rank]
                 r0 = int(cbs[shard.rank][c])
                 mine_c.copy_(local_spmv(x, r0, r0 + mine_c.numel()) if chunks > 1 else local_spmv(x))
-                works.append(dist.all_gather(views[c], mine_c, group=group, async_op=True))
+                try:
+                    works.append(dist.all_gather(views[c], mine_c, group=group, async_op=True))
+                except (RuntimeError, ValueError):   # no uneven all_gather: equal-size pieces
+                    _UNEVEN_OK[0] = False
+                    w = max(v.numel() for v in views[c])
+                    tmp = torch.zeros(world * w, dtype=x.dtype, device=x.device)
+                    pad = torch.zeros(w, dtype=x.dtype, device=x.device)
+                    pad[: mine_c.numel()].copy_(mine_c)
+                    dist.all_gather_into_tensor(tmp, pad, group=group)
+                    for r, v in enumerate(views[c]):
+                        v.copy_(tmp[r * w: r * w + v.numel()])
             for w in works:
                 w.wait()
             y = y_full
