@@ -80,6 +80,23 @@ typedef struct lw_probe {
     int32_t* atom_visits; /* [nnz] visit counter; caller zeroes it              */
 } lw_probe_t;
 
+/* Debug / introspection entry points over the probe: run the
+ * instrumented SpMV of `schedule` (LW_THREAD_MAPPED / LW_MERGE_PATH /
+ * LW_GROUP_MAPPED) into y and return per_lane_out[lanes] = atoms per lane
+ * (executor.imbalance's per_lane_atoms), or atom_lane_out / atom_tile_out[nnz]
+ * (the lane and tile of every atom, as execute_tile_major /
+ * execute_merge_path assign them; either may be NULL). lanes = 0 selects
+ * lw_auto_lanes(); the work_oriented schedule needs `workspace`
+ * (lw_spmv_workspace). */
+int lw_debug_lane_atom_counts(int schedule, const struct lw_csr* A, const void* x, void* y,
+                              int64_t lanes, int64_t group_size, int64_t tiles_per_block,
+                              int64_t* per_lane_out, void* workspace, size_t workspace_bytes,
+                              uintptr_t stream);
+int lw_debug_atom_tiles(int schedule, const struct lw_csr* A, const void* x, void* y, int64_t lanes,
+                        int64_t group_size, int64_t tiles_per_block, int32_t* atom_lane_out,
+                        int32_t* atom_tile_out, void* workspace, size_t workspace_bytes,
+                        uintptr_t stream);
+
 /* ---- library / device queries --------------------------------------------- */
 const char* lw_error_string(int code);
 int lw_abi_version(void);

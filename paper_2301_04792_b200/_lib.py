@@ -47,6 +47,8 @@ EXPORTS = (
     "lw_spmv_work_oriented_hotx_workspace",
     "lw_spmv_work_oriented_hotx",
     "lw_spmv_work_oriented_hotx_phases",
+    "lw_debug_lane_atom_counts",
+    "lw_debug_atom_tiles",
     "lw_norm_workspace",
     "lw_vector_norm",
     "lw_vector_scale",
@@ -148,6 +150,10 @@ _SIGNATURES = {
     "lw_spmv_work_oriented_hotx": (ctypes.c_int, [_csr_p, _vp, _i32, _vp, _vp, _i64, _vp, _sz, _up]),
     "lw_spmv_work_oriented_hotx_phases": (ctypes.c_int, [_csr_p, _vp, _i32, _vp, _vp, _i64, _vp, _sz,
                                                          _u32, _up]),
+    "lw_debug_lane_atom_counts": (ctypes.c_int, [ctypes.c_int, _csr_p, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _sz,
+                                                 _up]),
+    "lw_debug_atom_tiles": (ctypes.c_int, [ctypes.c_int, _csr_p, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _sz,
+                                           _up]),
     "lw_norm_workspace": (_sz, [_i64]),
     "lw_vector_norm": (ctypes.c_int, [_vp, _i64, _i32, _vp, _sz, _vp, _up]),
     "lw_vector_scale": (ctypes.c_int, [_vp, _i64, _i32, _vp, _vp, _up]),

@@ -256,6 +256,34 @@ int lw_spmv_group_mapped(const lw_csr_t* A, const void* x, void* y, int64_t lane
     return spmv_group_mapped(A, x, y, p, gs, tpb, probe, (cudaStream_t)stream);
 }
 
+// ---- debug / introspection over the probe ----------------------------
+static int debug_probe_run(int schedule, const lw_csr_t* A, const void* x, void* y, int64_t lanes,
+                           int64_t gs, int64_t tpb, const lw_probe_t* pr, void* ws, size_t ws_bytes,
+                           uintptr_t stream) {
+    switch (schedule) {
+        case LW_THREAD_MAPPED: return lw_spmv_thread_mapped(A, x, y, lanes, pr, stream);
+        case LW_MERGE_PATH: return lw_spmv_work_oriented(A, x, y, lanes, ws, ws_bytes, pr, stream);
+        case LW_GROUP_MAPPED: return lw_spmv_group_mapped(A, x, y, lanes, gs, tpb, pr, stream);
+        default: return LW_E_INVALID_ARG;
+    }
+}
+
+int lw_debug_lane_atom_counts(int schedule, const lw_csr_t* A, const void* x, void* y, int64_t lanes,
+                              int64_t gs, int64_t tpb, int64_t* per_lane_out, void* ws, size_t ws_bytes,
+                              uintptr_t stream) {
+    if (!per_lane_out) return LW_E_INVALID_ARG;
+    lw_probe_t pr{per_lane_out, nullptr, nullptr, nullptr};
+    return debug_probe_run(schedule, A, x, y, lanes, gs, tpb, &pr, ws, ws_bytes, stream);
+}
+
+int lw_debug_atom_tiles(int schedule, const lw_csr_t* A, const void* x, void* y, int64_t lanes, int64_t gs,
+                        int64_t tpb, int32_t* atom_lane_out, int32_t* atom_tile_out, void* ws, size_t ws_bytes,
+                        uintptr_t stream) {
+    if (!atom_lane_out && !atom_tile_out) return LW_E_INVALID_ARG;
+    lw_probe_t pr{nullptr, atom_lane_out, atom_tile_out, nullptr};
+    return debug_probe_run(schedule, A, x, y, lanes, gs, tpb, &pr, ws, ws_bytes, stream);
+}
+
 size_t lw_spmv_workspace(int schedule, int64_t rows, int64_t nnz, int64_t lanes, int32_t dtype) {
     return schedule == LW_MERGE_PATH ? lw_spmv_work_oriented_workspace(rows, nnz, lanes, dtype) : 0;
 }

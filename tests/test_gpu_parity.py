@@ -10,6 +10,8 @@ reference itself (tests/golden) or (b) the C oracle on the same seeded inputs:
     1e-12 (fp64), the north star's tolerance (BASELINE.json).
 """
 
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -557,3 +559,40 @@ def test_group_warp_staged_and_cooperative_blocks_bit_exact(dtype):
     for lanes in (None, 32 * 700, 32 * 5000):
         np.testing.assert_array_equal(run(m, x, "group-mapped", lanes, 32, 32), want,
                                       err_msg=f"lanes={lanes}")
+
+
+@pytest.mark.parametrize("kind,gs", [("thread-mapped", 32), ("merge-path", 32), ("group-mapped", 32),
+                                     ("group-mapped", 256), ("group-mapped", 4)])
+def test_debug_entry_points_match_the_probe(kind, gs):
+    """lw_debug_lane_atom_counts / lw_debug_atom_tiles (SURVEY §8(b)'s named
+    introspection calls) return what the probe records, and the per-lane counts
+    equal the reference's imbalance() at the launch's lane count."""
+    from paper_2301_04792_b200 import _lib
+    from paper_2301_04792_b200.device import current_stream
+
+    m = lwb.generate_power_law_csr(3000, 9.0, 1.3, seed=4)
+    dm = m.to_device("float64")
+    x = torch.as_tensor(np.random.default_rng(1).random(m.cols), device="cuda")
+    cfg = ExecutorConfig(schedule=ScheduleKind(kind), lanes=97 if kind != "group-mapped" else 4 * gs,
+                         group_size=gs, tiles_per_block=gs)
+    _, pr, lanes = lwb.spmv_probe(dm, x, cfg)
+    lib = _lib.load()
+    code = {"thread-mapped": _lib.LW_THREAD_MAPPED, "merge-path": _lib.LW_MERGE_PATH,
+            "group-mapped": _lib.LW_GROUP_MAPPED}[kind]
+    need = lib.lw_spmv_workspace(code, m.rows, m.nnz, lanes, _lib.LW_F64)
+    ws = torch.empty(max(need, 1), dtype=torch.uint8, device="cuda")
+    y = torch.empty(m.rows, dtype=torch.float64, device="cuda")
+    per_lane = torch.zeros(lanes, dtype=torch.int64, device="cuda")
+    a_lane = torch.full((m.nnz,), -1, dtype=torch.int32, device="cuda")
+    a_tile = torch.full((m.nnz,), -1, dtype=torch.int32, device="cuda")
+    s = current_stream(dm.device)
+    A = dm.c_struct()
+    _lib.check(lib.lw_debug_lane_atom_counts(code, A, x.data_ptr(), y.data_ptr(), lanes, gs, gs,
+                                             per_lane.data_ptr(), ws.data_ptr(), need, s), "debug counts")
+    _lib.check(lib.lw_debug_atom_tiles(code, A, x.data_ptr(), y.data_ptr(), lanes, gs, gs, a_lane.data_ptr(),
+                                       a_tile.data_ptr(), ws.data_ptr(), need, s), "debug tiles")
+    np.testing.assert_array_equal(per_lane.cpu().numpy(), pr["lane_atoms"])
+    np.testing.assert_array_equal(a_lane.cpu().numpy(), pr["atom_lane"])
+    np.testing.assert_array_equal(a_tile.cpu().numpy(), pr["atom_tile"])
+    rep = lwb.imbalance(lwb.csr_tile_set(m), dataclasses.replace(cfg, lanes=lanes))
+    np.testing.assert_array_equal(per_lane.cpu().numpy(), rep.per_lane_atoms)
