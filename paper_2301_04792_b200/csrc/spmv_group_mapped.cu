@@ -84,12 +84,53 @@ __device__ __forceinline__ void load_steps(const Csr<OffT, ValT>& A, int64_t bas
 template <class ValT, int U, int STRIDE, class OffT>
 __device__ __forceinline__ void gather_loaded(const StepLoads<ValT, U>& L, const ValT* __restrict__ x,
                                               OffT k0, int m, OffT total, double (&p)[U]) {
+    // every gather issued before the first product: written as one expression
+    // per step, ptxas placed each product right after its gather and the warp
+    // waited out U round trips per iteration (C3 fp32 11.9 -> 10.2 ms, power-law
+    // skew 1.05 3.87 -> 2.85 ms with the split)
+    ValT g[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-        const bool valid = k0 + u * STRIDE + m < total;
-        p[u] = valid ? (double)L.v[u] * (double)ld_gather(x + L.c[u]) : 0.0;
-    }
+    for (int u = 0; u < U; ++u) g[u] = k0 + u * STRIDE + m < total ? ld_gather(x + L.c[u]) : (ValT)0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) p[u] = (double)L.v[u] * (double)g[u];
 }
+
+// Cooperative-path iterations whose atoms all fall in one tile (the inside of a
+// long row): each lane adds its products to a running fp64 sum, and the warp
+// reduces it (fixed xor-butterfly order) into the tile's accumulator once, when
+// the run of single-tile iterations ends. Warp-uniform state.
+// Block tiles: 1 = one block-uniform get_tile(k0) per iteration decides (C3 fp32 /
+// fp64 8.37 / 9.90 -> 5.36 / 7.06 ms, power-law skew 1.05 1.21 / 1.40 -> 0.66 /
+// 0.87; C1 +6% / +13%: ~10 rows per iteration never qualify); 2 = a warp vote
+// over the per-atom searches it already does (C3 8.03 ms: the searches are the
+// cost); 0 = off. Gating the check on a block-wide "has a row >= GU*NT atoms"
+// flag cost the loop its register allocation (C3 6.82 ms).
+#ifndef LW_G_SINGLE
+#define LW_G_SINGLE 1
+#endif
+#ifndef LW_GW_SINGLE    // warp tiles: fp32 power-law -15% but fp64 C3 11.4 -> 17.2 ms and C2b
+#define LW_GW_SINGLE 0  // +12% (63 registers, fewer resident groups), off
+#endif
+struct SingleTileRun {
+    double sum = 0.0;
+    int tile = -1;
+    template <int U>
+    __device__ __forceinline__ void take(int t, const double (&p)[U], int lane, double* acc) {
+        if (t != tile) { flush(lane, acc); tile = t; }
+#pragma unroll
+        for (int u = 0; u < U; ++u) sum += p[u];
+    }
+    __device__ __forceinline__ void flush(int lane, double* acc) {
+        if (tile < 0) return;
+        double r = sum;
+#pragma unroll
+        for (int d = kWarp / 2; d >= 1; d >>= 1) r += __shfl_xor_sync(0xffffffffu, r, d);
+        if (lane == 0) acc[tile] += r;
+        __syncwarp();
+        sum = 0.0;
+        tile = -1;
+    }
+};
 
 // ---- warp tiles -------------------------------------------------------------------
 #ifndef LW_GW_CAP      // atoms per warp block staged in shared memory (0 = off)
@@ -165,12 +206,32 @@ __device__ __forceinline__ void group_warp_coop(const Csr<OffT, ValT>& A, const 
       constexpr int U = decltype(uc)::value;
       StepLoads<ValT, U> cur, nxt;
       if (U > 1) load_steps<ValT, U, kWarp>(A, base, (OffT)0, lane, total, cur);
+      SingleTileRun run;
       for (OffT k0 = 0; k0 < total; k0 += U * kWarp) {
         double p[U];
         if (U > 1) {   // long block: next steps' loads overlap these gathers
             load_steps<ValT, U, kWarp>(A, base, (OffT)(k0 + U * kWarp), lane, total, nxt);
             gather_loaded<ValT, U, kWarp>(cur, x, k0, lane, total, p);
             cur = nxt;
+          if (LW_GW_SINGLE) {
+            // every atom of the iteration in one tile (inside a long row): no
+            // get_tile search and no segmented reductions, the products go to a
+            // per-lane running sum that is reduced once when the run of such
+            // iterations ends (deterministic order)
+            // get_tile(k0): the largest tile starting at or before k0 (one ballot)
+            const int t0 = 31 - __clz(__ballot_sync(0xffffffffu, lane < tc && excl <= k0));
+            const OffT last = k0 + (OffT)(U * kWarp) < total ? k0 + (OffT)(U * kWarp) : total;
+            if (shfl((OffT)(excl + cnt), t0) >= last) {
+                run.take<U>(t0, p, lane, acc);
+                if (PROBE) {
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (k0 + u * kWarp + lane < total) { probe_atom(probe, base + k0 + u * kWarp + lane, glane, tb + t0); ++mine; }
+                }
+                continue;
+            }
+            run.flush(lane, acc);
+          }
         } else {
             gather_steps<ValT, U, kWarp>(A, x, base, k0, lane, total, p);
         }
@@ -218,6 +279,7 @@ __device__ __forceinline__ void group_warp_coop(const Csr<OffT, ValT>& A, const 
         }
         t_cur = t_next;
       }
+      run.flush(lane, acc);
     };
     if (total >= (OffT)(GU_LONG * kWarp)) steps(std::integral_constant<int, GU>{});
     else steps(std::integral_constant<int, 1>{});
@@ -437,20 +499,59 @@ __global__ void __launch_bounds__(NT, MODE == GB_FUSED ? LW_GB_MINB * 256 / NT :
         // occupancy step on short rows, 0.22 -> 0.25 ms on C2u, so it stays plain)
         auto steps = [&](auto uc) {
           constexpr int U = decltype(uc)::value;
+          SingleTileRun run;
           for (OffT k0 = 0; k0 < total; k0 += U * NT) {
             double p[U];
             gather_steps<ValT, U, NT>(A, x, base, k0, tid, total, p);
+            if (LW_G_SINGLE == 1 && U > 1) {   // single-tile iteration (inside a long row)
+                int t0 = 0;
+#pragma unroll
+                for (int s = NT / 2; s >= 1; s >>= 1)
+                    if (t0 + s < tc && s_excl[t0 + s] <= k0) t0 += s;
+                const OffT end = t0 + 1 < tc ? s_excl[t0 + 1] : total;
+                const OffT last = k0 + (OffT)(U * NT) < total ? k0 + (OffT)(U * NT) : total;
+                if (end >= last) {
+                    run.take<U>(t0, p, lane, s_acc[warp]);
+                    if (PROBE) {
+#pragma unroll
+                        for (int u = 0; u < U; ++u)
+                            if (k0 + u * NT + tid < total) { probe_atom(probe, base + k0 + u * NT + tid, glane, tb + t0); ++mine; }
+                    }
+                    continue;
+                }
+                run.flush(lane, s_acc[warp]);
+            }
+            int ts[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const OffT k = k0 + u * NT + tid;
-                const bool valid = k < total;
                 int t = 0;
-                if (valid) {
+                if (k < total) {
 #pragma unroll
                     for (int s = NT / 2; s >= 1; s >>= 1)
                         if (t + s < tc && s_excl[t + s] <= k) t += s;
                 }
-                if (PROBE && valid) { probe_atom(probe, base + k, glane, tb + t); ++mine; }
+                ts[u] = t;
+                if (PROBE && k < total) { probe_atom(probe, base + k, glane, tb + t); ++mine; }
+            }
+            if (LW_G_SINGLE == 2 && U > 1) {
+                // this warp's atoms of the iteration all in one tile (inside a long
+                // row): no segmented reductions, a per-lane running sum instead
+                const int tt = shfl(ts[0], 0);
+                bool same = true;
+#pragma unroll
+                for (int u = 0; u < U; ++u) same = same && (k0 + u * NT + tid >= total || ts[u] == tt);
+                if (__all_sync(0xffffffffu, same)) {
+                    run.take<U>(tt, p, lane, s_acc[warp]);
+                    continue;
+                }
+                run.flush(lane, s_acc[warp]);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const OffT k = k0 + u * NT + tid;
+                const bool valid = k < total;
+                const int t = ts[u];
                 const int key = valid ? t : INT_MAX;
                 const int prev = shfl_up(key, 1);
                 const bool head = lane == 0 || prev != key;
@@ -461,6 +562,7 @@ __global__ void __launch_bounds__(NT, MODE == GB_FUSED ? LW_GB_MINB * 256 / NT :
                 __syncwarp();
             }
           }
+          run.flush(lane, s_acc[warp]);
         };
         if (total >= (OffT)(GU_LONG * NT)) steps(std::integral_constant<int, GU>{});
         else steps(std::integral_constant<int, 1>{});

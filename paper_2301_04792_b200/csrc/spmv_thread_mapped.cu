@@ -15,6 +15,15 @@
 #ifndef LW_TM_UV
 #define LW_TM_UV 4   // vectors in flight per thread on long rows
 #endif
+// rows of >= LW_TM_LONG * UV vectors take the pipelined loop: 48 atoms fp32, 16
+// fp64 (8 / 8: C1 fp32 0.0246 -> 0.0164 ms, C2u fp64 0.235 -> 0.192, C2b fp32
+// unchanged at 3 and +7% at 2)
+#ifndef LW_TM_LONG
+#define LW_TM_LONG 3
+#endif
+#ifndef LW_TM_LONG64
+#define LW_TM_LONG64 2
+#endif
 
 namespace lw {
 
@@ -75,7 +84,7 @@ __device__ __forceinline__ double row_dot(const int32_t* __restrict__ col,
         // so a single thread keeps UV*V gathers in flight (the thread-mapped
         // schedule puts whole long rows on one thread)
         constexpr int UV = LW_TM_UV;
-        if (e - b >= 8 * UV * V) {   // only long rows; short rows keep the plain loop below
+        if (e - b >= (sizeof(ValT) == 4 ? LW_TM_LONG : LW_TM_LONG64) * UV * V) {   // only long rows; short rows keep the plain loop below
             // software pipeline: the next group's col_idx / values stream in
             // while this group's gathers are in flight, so a step costs one
             // round trip (the gathers) instead of two

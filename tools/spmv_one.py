@@ -1,7 +1,7 @@
 """A few back-to-back SpMVs of one BASELINE workload under one schedule, for an ncu
 capture of that schedule's kernel (the bench_sweep matrices, same generators).
 
-    python tools/spmv_one.py C2b group_block [fp32|fp64] [reps]
+    python tools/spmv_one.py C2b group_block [fp32|fp64] [reps]     (C4 skew s: C4s<s>)
     schedules: thread_mapped, work_oriented, work_oriented_hot, group_warp, group_block
 """
 import sys
@@ -24,6 +24,8 @@ def matrix(name, dt):
         return lw.generate_banded_device(1_000_000, 16, seed=2, dtype=dt)
     if name == "C2u":
         return lw.generate_uniform_device(1_000_000, 1_000_000, 32_000_000, seed=2, dtype=dt)
+    if name.startswith("C4s"):   # C4 power-law matrix of the given skew, e.g. C4s1.05
+        return lw.generate_power_law_csr(1 << 20, 16.0, float(name[3:]), seed=4).to_device(dt)
     if name == "C3":
         return lw.generate_rmat_csr(24, 16, seed=3, dtype=dt)
     raise SystemExit(f"unknown workload {name}")
