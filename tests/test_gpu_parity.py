@@ -246,6 +246,36 @@ def test_all_positive_long_rows_fp32():
         check_tol(run(m, x, kind), off, col, val, x, torch.float32)
 
 
+@pytest.mark.parametrize("gs", [256, 128, 64, 32])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_group_tiles_long_row_runs(gs, dtype):
+    """Blocks whose iterations fall inside one long row (the block tile's
+    single-tile path): runs starting and ending on iteration boundaries, runs
+    broken by short rows, one row spanning many iterations, empty rows between.
+    Integer data bit-exact against the oracle, float data within the bound and
+    bit-identical from run to run."""
+    rng = np.random.default_rng(21)
+    lens = rng.integers(0, 6, size=3 * gs)
+    lens[[0, 3, 5, gs - 1, gs, gs + 2]] = [5000, 1024, 1025, 4 * 1024 * (gs // 64 or 1), 2048, 100_000]
+    lens[gs + 1] = 0
+    cols = 5000
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    col = np.concatenate([np.sort(rng.choice(cols, size=int(n), replace=n > cols)) for n in lens if n])
+    for integer in (True, False):
+        val = (rng.integers(-3, 4, size=col.size).astype(np.float64) if integer
+               else rng.random(col.size) * 2 - 1)
+        x = rng.integers(-3, 4, size=cols).astype(np.float64) if integer else rng.random(cols)
+        if dtype == torch.float32:
+            val, x = val.astype(np.float32).astype(np.float64), x.astype(np.float32).astype(np.float64)
+        m = dev_csr(off, col, val, cols, dtype)
+        y = run(m, x, "group-mapped", None, gs, gs)
+        if integer:
+            np.testing.assert_array_equal(y, oracle.spmv(off, col, val, x, "thread-mapped", lanes=1))
+        else:
+            check_tol(y, off, col, val, x, dtype)
+            np.testing.assert_array_equal(y, run(m, x, "group-mapped", None, gs, gs))
+
+
 # ---- edge cases the reference tests -------------------------------------------------------
 
 @pytest.mark.parametrize("kind", ["thread-mapped", "merge-path", "group-mapped"])
