@@ -21,6 +21,9 @@
 #ifndef LW_TM_LONG
 #define LW_TM_LONG 3
 #endif
+#ifndef LW_TM_WIDE   // A/B: the few-lanes instantiation with 2*UV vectors in flight
+#define LW_TM_WIDE 1
+#endif
 #ifndef LW_TM_LONG64
 #define LW_TM_LONG64 2
 #endif
@@ -68,7 +71,7 @@ __device__ __forceinline__ void accum_vec<double>(const double2& v, const int2& 
 }
 
 // Dot product of row atoms [b, e) with x, fp64 accumulation in two chains.
-template <class ValT, bool VEC>
+template <class ValT, bool VEC, int UV, int LONG>
 __device__ __forceinline__ double row_dot(const int32_t* __restrict__ col,
                                           const ValT* __restrict__ val,
                                           const ValT* __restrict__ x, int64_t b, int64_t e) {
@@ -83,8 +86,7 @@ __device__ __forceinline__ double row_dot(const int32_t* __restrict__ col,
         // long rows: UV vectors per step, every load issued before the first use,
         // so a single thread keeps UV*V gathers in flight (the thread-mapped
         // schedule puts whole long rows on one thread)
-        constexpr int UV = LW_TM_UV;
-        if (e - b >= (sizeof(ValT) == 4 ? LW_TM_LONG : LW_TM_LONG64) * UV * V) {   // only long rows; short rows keep the plain loop below
+        if (e - b >= LONG * UV * V) {   // only long rows; short rows keep the plain loop below
             // software pipeline: the next group's col_idx / values stream in
             // while this group's gathers are in flight, so a step costs one
             // round trip (the gathers) instead of two
@@ -124,7 +126,10 @@ __device__ __forceinline__ double row_dot(const int32_t* __restrict__ col,
     return a0 + a1;
 }
 
-template <class OffT, class ValT, bool VEC, bool PROBE>
+// UV / LONG: vectors in flight per thread on rows of >= LONG*UV vectors. The sums
+// do not depend on them (atoms are accumulated in order into the same two chains).
+template <class OffT, class ValT, bool VEC, bool PROBE, int UV = LW_TM_UV,
+          int LONG = (sizeof(ValT) == 4 ? LW_TM_LONG : LW_TM_LONG64)>
 __global__ void __launch_bounds__(256)
     k_spmv_thread_mapped(Csr<OffT, ValT> A, const ValT* __restrict__ x,
                          ValT* __restrict__ y, int64_t lanes, Probe probe) {
@@ -133,7 +138,7 @@ __global__ void __launch_bounds__(256)
     int64_t mine = 0;
     for (int64_t t = lane; t < A.rows; t += lanes) {
         const int64_t b = ld_off(A.off + t), e = ld_off(A.off + t + 1);
-        y[t] = (ValT)row_dot<ValT, VEC>(A.col, A.val, x, b, e);
+        y[t] = (ValT)row_dot<ValT, VEC, UV, LONG>(A.col, A.val, x, b, e);
         if (PROBE) {
             mine += e - b;
             for (int64_t a = b; a < e; ++a) probe_atom(probe, a, lane, t);
@@ -147,7 +152,16 @@ int launch_thread_mapped(const lw_csr_t* A, const void* x, void* y, int64_t lane
                          const lw_probe_t* probe, cudaStream_t s) {
     Csr<OffT, ValT> a{A->rows, A->cols, A->nnz, (const OffT*)A->row_offsets,
                       A->col_indices, (const ValT*)A->values};
-    constexpr int NT = 256;
+    // CTA size: 256 threads, or fewer when that leaves SMs idle — each lane is one
+    // thread whatever the CTA size (same rows, same sums), but the lanes' gathers
+    // then issue from every SM's L1 instead of a few (C1: 10 K lanes are 40 CTAs
+    // of 256 on 40 of 148 SMs; at 64 they spread over all of them)
+#ifndef LW_TM_SPREAD
+#define LW_TM_SPREAD 1
+#endif
+    int NT = 256;
+    if (LW_TM_SPREAD)
+        while (NT > 32 && ceil_div(lanes, (int64_t)NT) < 2 * (int64_t)sm_count()) NT >>= 1;
     const int64_t grid = ceil_div(lanes, NT);
     if (grid > 0x7fffffff) return LW_E_UNSUPPORTED;
     const bool vec = ((uintptr_t)A->values % 16 == 0) && ((uintptr_t)A->col_indices % 16 == 0);
@@ -157,6 +171,11 @@ int launch_thread_mapped(const lw_csr_t* A, const void* x, void* y, int64_t lane
     if (probe) {
         if (vec) k_spmv_thread_mapped<OffT, ValT, true, true><<<grid, NT, 0, s>>>(a, (const ValT*)x, (ValT*)y, lanes, p);
         else     k_spmv_thread_mapped<OffT, ValT, false, true><<<grid, NT, 0, s>>>(a, (const ValT*)x, (ValT*)y, lanes, p);
+    } else if (vec && LW_TM_WIDE && lanes <= (int64_t)sm_count() * 128) {
+        // few lanes (C1: 10 K rows): occupancy is not the limit, the per-thread
+        // chain of gather round trips is, so each thread keeps twice the vectors
+        // in flight from 2 groups on (same sums)
+        k_spmv_thread_mapped<OffT, ValT, true, false, 2 * LW_TM_UV, 2><<<grid, NT, 0, s>>>(a, (const ValT*)x, (ValT*)y, lanes, p);
     } else {
         if (vec) k_spmv_thread_mapped<OffT, ValT, true, false><<<grid, NT, 0, s>>>(a, (const ValT*)x, (ValT*)y, lanes, p);
         else     k_spmv_thread_mapped<OffT, ValT, false, false><<<grid, NT, 0, s>>>(a, (const ValT*)x, (ValT*)y, lanes, p);
