@@ -38,6 +38,9 @@ constexpr int WO_S = WO_W - 16;
 #ifndef LW_WO_PDL   // A/B: chunk and fix-up kernels as programmatic dependent launches
 #define LW_WO_PDL 1
 #endif
+#ifndef LW_WO_WARP_SEARCH   // partitions of at most this many boundaries use the warp-cooperative search
+#define LW_WO_WARP_SEARCH 12288
+#endif
 #ifndef LW_WO_BATCH   // A/B: batch the unpacked kernel's gathers like the packed one's
 #define LW_WO_BATCH 0
 #endif
@@ -117,6 +120,52 @@ __global__ void k_merge_path_search(const OffT* __restrict__ off, int64_t rows, 
     if (out_coords) {
         out_coords[2 * k] = lo;
         out_coords[2 * k + 1] = d - lo;
+    }
+}
+
+// Warp-cooperative form of the same search, for launches with few boundaries
+// (C1/C2/C4 sizes: a few thousand), where the per-thread binary search is a chain
+// of ~24 dependent L2 round trips and nothing else runs: each round the warp
+// probes 32 points of the remaining range and keeps the gap between the last
+// true and the first false probe (off[t] + t is strictly increasing, so the true
+// probes are a prefix), ~5 rounds instead of 24. Same result as the binary search
+// (the greatest t with off[t] <= d - t). With many boundaries (C3: 68.7 K) the 32x
+// probes make it request-bound, so launch_search keeps the per-thread search there.
+template <class OffT>
+__device__ __forceinline__ int64_t mp_search_warp(const OffT* __restrict__ off, int64_t d, int64_t rows,
+                                                  int64_t nnz, int lane) {
+    int64_t lo = max((int64_t)0, d - nnz), hi = min(d, rows);
+    while (lo < hi) {
+        const int64_t span = hi - lo;
+        const int64_t p = lo + ((int64_t)(lane + 1) * span + 31) / 32;   // in (lo, hi], p of lane 31 = hi
+        const unsigned m = __ballot_sync(0xffffffffu, ld_off(off + p) <= d - p);
+        const int k = __popc(m);
+        if (k == 32) return hi;
+        hi = lo + ((int64_t)(k + 1) * span + 31) / 32 - 1;                // before the first false probe
+        if (k) lo = lo + ((int64_t)k * span + 31) / 32;                   // the last true probe
+    }
+    return lo;
+}
+
+template <class OffT>
+__global__ void k_merge_path_search_warp(const OffT* __restrict__ off, int64_t rows, int64_t nnz,
+                                         int64_t n_bounds, int64_t J, int64_t items, int64_t S,
+                                         int64_t* __restrict__ out_tile,
+                                         int64_t* __restrict__ out_coords,
+                                         unsigned* __restrict__ ticket = nullptr) {
+    if (LW_WO_PDL) pdl_trigger();
+    const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & (kWarp - 1);
+    if (ticket && k == 0 && lane == 0) *ticket = 0u;
+    if (k >= n_bounds) return;   // warp-uniform
+    const int64_t d = wo_bound_diag(k, J, items, S, rows + nnz);
+    const int64_t t = mp_search_warp(off, d, rows, nnz, lane);
+    if (lane == 0) {
+        if (out_tile) out_tile[k] = t;
+        if (out_coords) {
+            out_coords[2 * k] = t;
+            out_coords[2 * k + 1] = d - t;
+        }
     }
 }
 
@@ -808,8 +857,12 @@ static int launch_search(const OffT* off, int64_t rows, int64_t nnz, int64_t n_b
                          int64_t items, int64_t S, int64_t* out_tile, int64_t* out_coords,
                          cudaStream_t s, unsigned* ticket = nullptr) {
     const int NT = 256;
-    k_merge_path_search<OffT><<<ceil_div(n_bounds, NT), NT, 0, s>>>(off, rows, nnz, n_bounds, J, items,
-                                                                 S, out_tile, out_coords, ticket);
+    if (n_bounds <= LW_WO_WARP_SEARCH)
+        k_merge_path_search_warp<OffT><<<ceil_div(n_bounds * kWarp, NT), NT, 0, s>>>(
+            off, rows, nnz, n_bounds, J, items, S, out_tile, out_coords, ticket);
+    else
+        k_merge_path_search<OffT><<<ceil_div(n_bounds, NT), NT, 0, s>>>(off, rows, nnz, n_bounds, J, items,
+                                                                     S, out_tile, out_coords, ticket);
     LW_LAUNCH_CHECK();
     return LW_OK;
 }
