@@ -91,6 +91,29 @@ def test_partition_every_diagonal_matches_reference_search(golden):
         np.testing.assert_array_equal(got, want)
 
 
+@pytest.mark.parametrize("bits", [32, 64])
+def test_partition_both_search_paths_match_oracle(bits):
+    """Partitions of <= 12288 boundaries take the warp-cooperative search, larger
+    ones the per-thread binary search (spmv_work_oriented.cu launch_search): both
+    sides of the threshold against the oracle's search (reference
+    schedules.py:63-110) on a skewed matrix with runs of empty rows and one row
+    of 300 K atoms."""
+    rng = np.random.default_rng(11)
+    lengths = np.minimum(rng.zipf(1.4, 200_000) - 1, 5000)
+    lengths[50_000:90_000] = 0
+    lengths[120_000] = 300_000
+    off = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64)
+    nnz = int(off[-1])
+    odt = torch.int32 if bits == 32 else torch.int64
+    m = DeviceCsr(len(off) - 1, 1, torch.as_tensor(off).to("cuda", odt),
+                  torch.zeros(nnz, dtype=torch.int32, device="cuda"),
+                  torch.zeros(nnz, dtype=torch.float32, device="cuda"))
+    for p in (1, 7, 4096, 12287, 12288, 12289, 30_000):
+        want = oracle.merge_path_partition(off, p, threads=4)
+        got = lwb.device_merge_path_partition(m, p).cpu().numpy()
+        np.testing.assert_array_equal(got, want, err_msg=f"lanes={p}")
+
+
 def test_group_plan_prefix_matches_reference_golden(golden):
     g = golden["schedules"]
     k = 0
