@@ -117,7 +117,7 @@ def spmv(m, x, cfg: ExecutorConfig | None = None, *, out=None, dtype=None):
         raise ValueError(f"x has length {xh.size}, expected {m.cols}")
     dm = cached_device_csr(m, dtype=dtype or "float64")
     xd = host_to_device(xh, dm.device, dm.dtype)
-    if (cfg.schedule is ScheduleKind.MERGE_PATH and cfg.lanes_auto and dm.dtype == torch.float64
+    if (cfg.schedule in _OVERLAP_SCHEDULES and cfg.lanes_auto and dm.dtype == torch.float64
             and dm.nnz >= _OVERLAP_MIN_NNZ):
         return _spmv_host_overlapped(dm, m.row_offsets, xd, cfg)
     y = torch.empty(dm.rows, dtype=dm.dtype, device=dm.device)
@@ -131,18 +131,22 @@ def spmv(m, x, cfg: ExecutorConfig | None = None, *, out=None, dtype=None):
 # two, so it should start early and never wait: the blocks have equal rows (equal
 # download time) and run lightest first (fewest merge-path items = rows + atoms),
 # so the first download starts after the cheapest SpMV and every later block's
-# SpMV fits under the download before it. Only for the device-sized lane count:
-# each block is its own merge-path partition, so rows a lane boundary cuts may
-# add their partials in a different grouping than one whole-matrix launch (fp64,
-# far inside the 1e-12 bound; integer data stay bit-exact).
+# SpMV fits under the download before it. Only for the device-sized lane count,
+# and for the schedules whose row sums do not depend on where a launch starts:
+# thread_mapped (a row's atoms in order on one thread: y bit-identical) and
+# merge-path (each block is its own partition, so rows a lane boundary cuts may
+# add their partials in a different grouping than one whole-matrix launch: fp64,
+# far inside the 1e-12 bound; integer data stay bit-exact). group_mapped keeps
+# one launch: its member-major steps are aligned to each group's first atom.
 _OVERLAP_MIN_NNZ = 1 << 22
+_OVERLAP_SCHEDULES = (ScheduleKind.MERGE_PATH, ScheduleKind.THREAD_MAPPED)
 _OVERLAP_BLOCKS = 8
 _COPY_STREAMS = {}
 
 
 def _row_blocks(dm: DeviceCsr, host_offsets, parts: int):
-    """Equal-row blocks [(r0, r1, DeviceCsr view)] in increasing order of their
-    merge-path items, cached on the DeviceCsr while its tensors are unchanged."""
+    """(Nearly) equal-row blocks [(r0, r1, DeviceCsr view)] in increasing order of
+    their merge-path items, cached on the DeviceCsr while its tensors are unchanged."""
     from .device import _same_key
 
     key = dm._tensor_key()
@@ -150,7 +154,16 @@ def _row_blocks(dm: DeviceCsr, host_offsets, parts: int):
     if hit is not None and hit[0] == parts and _same_key(hit[1], key):
         return hit[2]
     off = np.asarray(host_offsets, dtype=np.int64)
-    bounds = np.unique(np.linspace(0, dm.rows, parts + 1).astype(np.int64))
+    bounds = np.linspace(0, dm.rows, parts + 1).astype(np.int64)
+    # move each inner bound to the next row whose first atom is 8-aligned, so every
+    # block's col_idx / values start on a 32-byte boundary (the kernels' vector
+    # loads need it; thread_mapped then also keeps its two chains bit-identical)
+    for i in range(1, parts):
+        near = off[bounds[i]: min(bounds[i] + 4096, dm.rows)]
+        hit = np.flatnonzero(near % 8 == 0)
+        if hit.size:
+            bounds[i] += hit[0]
+    bounds = np.unique(np.maximum.accumulate(bounds))
     items = (bounds[1:] - bounds[:-1]) + (off[bounds[1:]] - off[bounds[:-1]])
     blocks = [(int(bounds[i]), int(bounds[i + 1]), dm.row_slice(int(bounds[i]), int(bounds[i + 1])))
               for i in np.argsort(items, kind="stable")]

@@ -1,7 +1,7 @@
 """The host-operand SpMV's overlapped download (kernels._spmv_host_overlapped):
-spmv(CsrMatrix, ndarray) on a large matrix runs the merge-path SpMV in
-nnz-balanced row blocks and downloads each block's y while the next block
-computes. Checked against the C oracle (reference kernels.py:57-98): integer
+spmv(CsrMatrix, ndarray) on a large matrix runs the merge-path (or
+thread_mapped) SpMV in equal-row blocks, lightest first, and downloads each
+block's y while the later blocks compute. Checked against the C oracle (reference kernels.py:57-98): integer
 data bit-exact, real data within the north star's fp64 bound; ragged inputs
 (empty rows at the block bounds, one row holding most atoms) included."""
 
@@ -80,6 +80,28 @@ def test_overlapped_blocks_follow_rebinding(small_threshold):
     m.values = m.values * 2
     y2 = lw.spmv(m, x)
     np.testing.assert_array_equal(y2, 2 * y1)
+
+
+def test_overlapped_thread_mapped_is_bit_identical(small_threshold):
+    """thread_mapped row blocks: every row is one thread's ordered chain, so y
+    equals the single-launch y bit for bit (real-valued data)."""
+    import torch
+
+    import paper_2301_04792_b200 as lw
+
+    rng = np.random.default_rng(8)
+    m = _matrix(rng, 30_000, 20_000, rng.integers(0, 60, size=30_000), False)
+    x = rng.random(20_000)
+    cfg = lw.ExecutorConfig(schedule=lw.ScheduleKind.THREAD_MAPPED)
+    y = lw.spmv(m, x, cfg)
+    dm = next(iter(m.__dict__["_lw_device_cache"].values()))[1]
+    assert "_lw_row_blocks" in dm.__dict__
+    single = lw.spmv(dm, torch.as_tensor(x, device="cuda"), cfg).cpu().numpy()
+    np.testing.assert_array_equal(y, single)
+    want = oracle.spmv(m.row_offsets, m.col_indices, m.values, x, "thread-mapped", threads=4)
+    ok, worst = oracle.tolerance_ok(y, want, oracle.abs_row_sums(m.row_offsets, m.col_indices,
+                                                                 m.values, x), 1e-12)
+    assert ok, worst
 
 
 def test_explicit_lanes_and_fp32_keep_the_single_launch(small_threshold):
