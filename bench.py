@@ -381,6 +381,11 @@ def power_measure(args, world, rank, local, dev, scale, seed):
         for k in range(layout.chunks):
             _, _, r0, r1 = layout.slot(rank, k)
             Ak = A if (r0, r1) == (0, A.rows) else A.row_slice(r0, r1)
+            if Ak.nnz and (Ak.col_indices.data_ptr() % 32 or Ak.values.data_ptr() % 32):
+                # a view starting mid-sector would run the chunk kernel without its
+                # 32-byte vector loads: give the chunk its own aligned copy
+                Ak = lwb.DeviceCsr(Ak.rows, Ak.cols, Ak.row_offsets, Ak.col_indices.clone(),
+                                   Ak.values.clone())
             if hot:
                 Ak.pack_hot_columns(args.max_hot or None)
             slices[(r0, r1)] = Ak
