@@ -630,7 +630,7 @@ __global__ void __launch_bounds__(FX_NT)
     const bool head = in && (i == 0 || prev != key);
     const bool brk = in && (i == c0 || head);   // scan segment boundary
     const bool tail = in && next != key;
-    if (tid < 2) segs[2 * blockIdx.x + tid] = FixSeg{-2, 0.0};
+    if (tid < 2 && gridDim.x > 1) segs[2 * blockIdx.x + tid] = FixSeg{-2, 0.0};
 
     // segmented inclusive scan of v (segments start at brk) + "a head in my segment"
     double run = v;
@@ -665,6 +665,8 @@ __global__ void __launch_bounds__(FX_NT)
             segs[2 * blockIdx.x + (hh ? 1 : 0)] = FixSeg{key, run};
         }
     }
+    // one CTA: every run started and ended inside it (no pieces, no merge)
+    if (gridDim.x == 1) return;
     // the last CTA to finish adds the runs that cross CTAs, in path order
     __threadfence();
     __syncthreads();
